@@ -1,0 +1,207 @@
+/*
+ * gmt.h -- C ABI of libgmt: the matrix-free voxel geometric-multigrid hot
+ * path of GMT (arXiv 2604.26518) on NVIDIA B200 (sm_100a).
+ *
+ * The library solves the periodic cell problems of PAPER.md Sec. 3.1
+ * (Eq. 1-3) for every load case at once -- linear elasticity (3 dof/node,
+ * the 6 unit strains of App. F1) or steady heat conduction (1 dof/node, the
+ * 3 unit gradients of App. F2) -- with the matrix-free element-by-element
+ * (EBE) GMG V-cycle of Sec. 3.2 Alg. 1 / Sec. 4.4 Alg. 2 / Sec. 4.6, and
+ * evaluates the effective tensor C^H (App. F1/F2 "Effective Property
+ * Calculation").  Every arithmetic step runs in the library's own CUDA
+ * kernels; there is no CPU fallback.
+ *
+ * Conventions:
+ *  - Voxel grid of N^3 unit-cube trilinear hexahedra on the periodic torus
+ *    (Eq. 2); lengths in voxel units, |Omega| = N^3.
+ *  - Material field: N^3 per-voxel scales s_e >= 0 in [z][y][x] order
+ *    (x fastest).  s_e = 0 is void, 1 is the base material, other values
+ *    scale it (App. F3 Eq. C_e = (rho_min + rho^p) C_0 evaluated by the
+ *    caller).  GMT_U8 input is occupancy: byte != 0 -> s = 1.
+ *  - Nodal vectors at level l (resolution n_l = N / 2^l, l = 0 finest):
+ *    float32 [z][y][x][m][c], m = load case (6 elastic / 3 thermal),
+ *    c = component (3 / 1); n_l^3 * NRHS * DPN floats, contiguous.
+ *  - Voigt order (11,22,33,23,13,12), engineering shear.
+ *  - Inactive nodes (every incident voxel void) are outside the active set
+ *    (Sec. 4.1.1): smoothing and prolongation leave them untouched.
+ *
+ * Ownership: the library owns all memory it allocates; every pointer the
+ * caller passes is borrowed for the duration of the call only.  Pointers
+ * flagged GMT_DEVICE must be device pointers on the problem's device;
+ * GMT_HOST pointers may be pageable or pinned host memory.
+ *
+ * Asynchrony: compute entry points enqueue work on the problem's CUDA stream
+ * and return; entry points that return host values (norms, C^H, solution to
+ * host) synchronise that stream first.  gmt_sync() waits explicitly.
+ *
+ * Errors: every int-returning function returns GMT_OK (0) or a negative
+ * GMT_ERR_* code; gmt_last_error() returns a thread-local message.  A CUDA
+ * error inside a call is reported as GMT_ERR_CUDA and leaves the problem
+ * in an unspecified numeric state (destroy it).
+ */
+#ifndef GMT_H_
+#define GMT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GMT_API __attribute__((visibility("default")))
+#else
+#define GMT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMT_ABI_VERSION 1
+
+#define GMT_OK 0
+#define GMT_ERR_ARG (-1)     /* invalid argument */
+#define GMT_ERR_CUDA (-2)    /* CUDA runtime / launch error */
+#define GMT_ERR_STATE (-3)   /* call not valid in the problem's state */
+#define GMT_ERR_NOMEM (-4)   /* device allocation failed */
+#define GMT_ERR_NCCL (-5)    /* NCCL failure (distributed problems) */
+
+#define GMT_PHYSICS_ELASTIC 0 /* App. F1: 3 dof/node, 6 load cases */
+#define GMT_PHYSICS_THERMAL 1 /* App. F2: 1 dof/node, 3 load cases */
+
+#define GMT_F32 0 /* float32 scales */
+#define GMT_U8 1  /* uint8 occupancy */
+
+#define GMT_HOST 0
+#define GMT_DEVICE 1
+
+typedef struct gmt_problem_s* gmt_problem;
+
+typedef struct gmt_config {
+  int physics;        /* GMT_PHYSICS_* */
+  int res;            /* N_res voxels per axis; divisible by 2^(levels-1) */
+  int levels;         /* L >= 1 grid levels (Sec. 3.2); 0 = default: coarsest n >= 4 */
+  double E, nu;       /* base isotropic material (elastic); E > 0, -1 < nu < 0.5 */
+  double kappa;       /* base conductivity (thermal), > 0 */
+  double omega;       /* damped-Jacobi factor; 0 = default (0.45 elastic, 0.6 thermal) */
+  int pre_sweeps;     /* It^l pre-smoothing sweeps (Alg. 1 line 3); default 2 (App. A1) */
+  int post_sweeps;    /* It^l post-smoothing sweeps (Alg. 1 line 11); default 2 */
+  int coarse_sweeps;  /* It^L sweeps on the coarsest level (Alg. 1 line 8); default 16 */
+  int device;         /* CUDA device ordinal */
+  void* stream;       /* cudaStream_t to run on, or NULL: the library creates one */
+  int use_graphs;     /* 1 = replay V-cycles from a captured CUDA graph (default 1) */
+} gmt_config;
+
+/* Fill *cfg with defaults for the physics and resolution.  Returns GMT_ERR_ARG
+ * for unknown physics or res < 2. */
+GMT_API int gmt_default_config(gmt_config* cfg, int physics, int res);
+
+/* gmt_create -- the problem statement of PAPER.md Sec. 3.1: resolution,
+ * voxel material field and base material (E/nu or kappa).  Allocates the
+ * level hierarchy on cfg->device, uploads the material and builds the
+ * Galerkin coarse operators K^{l+1} = R K^l P (Sec. 3.2 "Operator
+ * Consistency", Sec. 4.6 Eq. 17).  The initial guess is zero.
+ *   material: N^3 voxel values [z][y][x] of material_dtype at material_location.
+ * Errors: GMT_ERR_ARG (bad config / null material), GMT_ERR_NOMEM, GMT_ERR_CUDA. */
+GMT_API int gmt_create(const gmt_config* cfg, const void* material, int material_dtype,
+               int material_location, gmt_problem* out);
+
+/* Replace the material field (same resolution) and rebuild the coarse
+ * operators; the solution is reset to zero. */
+GMT_API int gmt_set_material(gmt_problem p, const void* material, int dtype, int location);
+
+/* Alg. 2 line 1: u^1 <- u_hat^1.  u: finest-level vector (layout above) or
+ * NULL for zero. */
+GMT_API int gmt_set_initial_guess(gmt_problem p, const float* u, int location);
+
+/* Alg. 2 line 6: u^{l} <- e_hat^{l} instead of 0 for level l in [1, L-1]
+ * during the NEXT gmt_vcycle call only.  e: level-l vector or NULL to clear. */
+GMT_API int gmt_inject_correction(gmt_problem p, int level, const float* e, int location);
+
+/* Run ncycles V-cycles (Alg. 1 with damped-Jacobi smoothing) on the current
+ * solution for all load cases.  Asynchronous. */
+GMT_API int gmt_vcycle(gmt_problem p, int ncycles);
+
+/* Relative residual of Sec. 5.2, r_m = ||f_m - K u_m||_2 / ||f_m||_2, for each
+ * load case m of the current finest-level solution.  rel, abs_r, abs_f are
+ * host arrays of NRHS doubles (abs_r / abs_f may be NULL).  Synchronises. */
+GMT_API int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f);
+
+/* Repeat V-cycles until max_m r_m <= rel_tol or max_cycles cycles ran.
+ * *cycles_done / *final_rel (max over load cases) may be NULL; history, if
+ * non-NULL, receives (max_cycles+1)*NRHS doubles: per-cycle residuals,
+ * history[0..NRHS) being the initial one.  Synchronises.  Returns GMT_OK
+ * also when the tolerance was not reached (check *final_rel). */
+GMT_API int gmt_solve(gmt_problem p, double rel_tol, int max_cycles, int* cycles_done,
+              double* final_rel, double* history);
+
+/* App. F1/F2 effective tensor of the current solution:
+ *   C^H_ij = 1/|Omega| sum_e (x_0^i - u_e^i)^T (s_e K_e) (x_0^j - u_e^j)
+ * written row-major to CH (NRHS x NRHS host doubles: 6x6 C^H or 3x3 kappa^H).
+ * Synchronises. */
+GMT_API int gmt_homogenize(gmt_problem p, double* CH);
+
+/* Copy the finest-level solution to u (layout above).  zero_mean != 0
+ * applies the Sec. 4.5 gauge sum_i u_i = 0 per load case and component over
+ * the active nodes (to the copy only).  Synchronises when location==GMT_HOST. */
+GMT_API int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean);
+
+/* Problem properties. */
+GMT_API int gmt_num_levels(gmt_problem p);
+GMT_API int gmt_level_res(gmt_problem p, int level);      /* n_l */
+GMT_API int gmt_nrhs(gmt_problem p);                      /* 6 or 3 */
+GMT_API int gmt_dpn(gmt_problem p);                       /* 3 or 1 */
+GMT_API void* gmt_stream(gmt_problem p);                  /* the problem's cudaStream_t */
+GMT_API size_t gmt_device_bytes(gmt_problem p);           /* device memory held */
+GMT_API int gmt_sync(gmt_problem p);
+GMT_API void gmt_destroy(gmt_problem p);
+GMT_API const char* gmt_last_error(void);
+GMT_API int gmt_abi_version(void);
+
+/* ---- Live profiling (bench instrumentation) ----------------------------------
+ * Kernel classes: 0 level-0 damped-Jacobi sweep, 1 level-0 residual, 2 level-0
+ * prolongation+correction, 3 restriction 0->1, 4 all level>=1 operator /
+ * transfer kernels, 5 coarsest solve, 6 Galerkin setup, 7 C^H reduction.
+ * gmt_profile_enable(p, mask): bracket every launch of the classes in `mask`
+ * (bit c = class c) with CUDA events on the problem stream (also inside the
+ * captured V-cycle graph).  gmt_profile_collect synchronises and accumulates
+ * the elapsed times of all brackets recorded since the previous collect;
+ * gmt_profile_read returns the accumulated milliseconds and launch count of
+ * one class.  gmt_kernel_launches counts every libgmt kernel launch executed
+ * (graph replays included). */
+GMT_API int gmt_profile_enable(gmt_problem p, unsigned mask);
+GMT_API int gmt_profile_collect(gmt_problem p);
+GMT_API int gmt_profile_read(gmt_problem p, int cls, double* total_ms, long long* launches, int reset);
+GMT_API long long gmt_kernel_launches(gmt_problem p);
+
+/* ---- Row-level entry points (one step of the hot path each) ------------------
+ * Device pointers only (GMT_DEVICE); vectors in the level layout above;
+ * asynchronous on the problem's stream.  They use the problem's material and
+ * Galerkin operators but never touch its solution state. */
+
+/* Sec. 4.6 Eq. 14: y = K^l u (level 0: EBE from the material; l >= 1: the
+ * Galerkin operator). */
+GMT_API int gmt_op_apply(gmt_problem p, int level, const float* u, float* y);
+/* Alg. 1 line 4: r = f - K^l u; f == NULL at level 0 means the load vector. */
+GMT_API int gmt_op_residual(gmt_problem p, int level, const float* u, const float* f, float* r);
+/* One damped-Jacobi sweep: u_out = u + omega D^{-1} (f - K^l u) on active
+ * dofs, u_out = u elsewhere; f == NULL at level 0 means the load vector. */
+GMT_API int gmt_op_jacobi(gmt_problem p, int level, const float* u, const float* f, float* u_out);
+/* App. E2 restriction R = P^T: f_c (level+1) = R r (level). */
+GMT_API int gmt_op_restrict(gmt_problem p, int level, const float* r, float* fc);
+/* App. E2 prolongation + correction: u (level) += P e (level+1) on active
+ * fine nodes. */
+GMT_API int gmt_op_prolong_add(gmt_problem p, int level, const float* e, float* u);
+/* Eq. 3 load vector f = sum_e A_e^T s_e f_e at level 0. */
+GMT_API int gmt_op_loads(gmt_problem p, float* f);
+/* diag(K^l), layout [z][y][x][c] (n_l^3 * DPN floats). */
+GMT_API int gmt_op_diagonal(gmt_problem p, int level, float* d);
+/* The assembled Galerkin operator of level l >= 1 as a 27-point block
+ * stencil: S[((d*DPN + a)*DPN + b) * n_l^3 + node], d = (dx+1) + 3(dy+1) +
+ * 9(dz+1): coupling of dof a at node i to dof b at node i + d. */
+GMT_API int gmt_op_stencil(gmt_problem p, int level, float* S);
+/* C^H of an arbitrary finest-level field u (device); CH host NRHS^2 doubles. */
+GMT_API int gmt_op_effective_tensor(gmt_problem p, const float* u, double* CH);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMT_H_ */

@@ -1,0 +1,825 @@
+// libgmt: host orchestration of the voxel EBE-GMG V-cycle and the C ABI
+// declared in include/gmt.h.  One translation unit: the kernel headers are
+// included here so every template is instantiated next to its launcher.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gmt.h"
+#include "gmt_fem.h"
+#include "k_level.cuh"
+#include "k_reduce.cuh"
+#include "k_setup.cuh"
+
+using namespace gmt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(GMT_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+#define TRY(x)                \
+  do {                        \
+    int rc_ = (x);            \
+    if (rc_ != GMT_OK) return rc_; \
+  } while (0)
+
+struct LevelBuf {
+  int n = 0, nz = 0;
+  size_t nodes = 0;
+  float* u = nullptr;    // solution / coarse error
+  float* t = nullptr;    // Jacobi ping-pong partner
+  float* f = nullptr;    // right-hand side (levels >= 1)
+  float* r = nullptr;    // residual (levels < L-1)
+  float* S = nullptr;    // 27-point block stencil (levels >= 1)
+  float* Ke = nullptr;   // Galerkin element matrices (levels >= 2)
+  float* inj = nullptr;  // Alg. 2 injected correction
+  bool inj_pending = false;
+};
+
+struct Geo {
+  dim3 grid, block;
+  int nblk;
+};
+
+Geo geo(int n, int nz) {
+  const int bx = n < 32 ? n : 32;
+  const int by = 128 / bx;
+  Geo g;
+  g.block = dim3(bx, by, 1);
+  g.grid = dim3((n + bx - 1) / bx, (n + by - 1) / by, nz);
+  g.nblk = g.grid.x * g.grid.y * g.grid.z;
+  return g;
+}
+
+}  // namespace
+
+struct gmt_problem_s {
+  gmt_config cfg{};
+  int dpn = 3, nr = 6, V = 18, L = 1, N = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  float* s = nullptr;  // material scales [z][y][x]
+  std::vector<LevelBuf> lv;
+  ElementData ed{};
+  FineConsts fc{};
+  M1Consts m1{};
+  CHConsts chc{};
+  WConsts wc{};
+  float* M1g = nullptr;
+  double* part = nullptr;
+  size_t part_cap = 0;   // doubles
+  double* red = nullptr; // device reduction results
+  double* hred = nullptr;  // pinned host mirror
+  uint8_t* u8tmp = nullptr;
+  size_t bytes = 0;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_ok = false;
+  // kernel accounting and live profiling
+  long long launches = 0;         // kernels executed (graph replays included)
+  long long capture_count = 0;    // kernels recorded into the graph being captured
+  long long graph_kernels = 0;    // kernels per V-cycle graph replay
+  bool capturing = false;
+  unsigned prof_mask = 0;
+  struct Pair { int cls; cudaEvent_t a, b; };
+  std::vector<cudaEvent_t> pool;   // transient brackets, recycled at each collect
+  std::vector<cudaEvent_t> gpool;  // brackets owned by the captured V-cycle graph
+  size_t pool_next = 0;
+  std::vector<Pair> pending, graph_pairs;
+  double prof_ms[8] = {0};
+  long long prof_cnt[8] = {0};
+
+  ZMap zm(int l) const { return ZMap{lv[l].nz, 1}; }
+};
+
+namespace {
+
+int dalloc(gmt_problem p, void** ptr, size_t bytes) {
+  if (bytes == 0) { *ptr = nullptr; return GMT_OK; }
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GMT_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  p->bytes += bytes;
+  return GMT_OK;
+}
+
+int set_device(gmt_problem p) {
+  CK(cudaSetDevice(p->cfg.device));
+  return GMT_OK;
+}
+
+// ---------------------------------------------------------------- accounting
+
+void note_launch(gmt_problem p) {
+  if (p->capturing) ++p->capture_count;
+  else ++p->launches;
+}
+
+cudaEvent_t pool_event(gmt_problem p) {
+  cudaEvent_t e = nullptr;
+  if (p->capturing) {
+    cudaEventCreate(&e);
+    p->gpool.push_back(e);
+    return e;
+  }
+  if (p->pool_next < p->pool.size()) return p->pool[p->pool_next++];
+  cudaEventCreate(&e);
+  p->pool.push_back(e);
+  p->pool_next = p->pool.size();
+  return e;
+}
+
+// Bracket one launch of class `cls` with events when profiling that class.
+struct Prof {
+  gmt_problem p;
+  int cls;
+  cudaEvent_t a = nullptr;
+  Prof(gmt_problem p_, int c) : p(p_), cls(c) {
+    if (p->prof_mask & (1u << cls)) {
+      a = pool_event(p);
+      cudaEventRecordWithFlags(a, p->stream, p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+    }
+  }
+  ~Prof() {
+    if (!a) return;
+    cudaEvent_t b = pool_event(p);
+    cudaEventRecordWithFlags(b, p->stream, p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+    (p->capturing ? p->graph_pairs : p->pending).push_back({cls, a, b});
+  }
+};
+
+#define LAUNCHED(p) \
+  do {              \
+    CKL();          \
+    note_launch(p); \
+  } while (0)
+
+// ---------------------------------------------------------------- launches
+
+template <int DPN>
+int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part) {
+  const LevelBuf& b = p->lv[l];
+  const Geo g = geo(b.n, b.nz);
+  cudaStream_t st = p->stream;
+  const float om = (float)p->cfg.omega;
+  Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
+  if (l == 0) {
+    const ZMap z = p->zm(0);
+    switch (mode) {
+      case M_APPLY: k_fine<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      case M_RESID: k_fine<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      case M_JACOBI: k_fine<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      case M_LOADS: k_fine<DPN, M_LOADS><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      case M_DIAG: k_fine<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      default: return fail(GMT_ERR_ARG, "bad mode");
+    }
+  } else {
+    const ZMap z = p->zm(l);
+    switch (mode) {
+      case M_APPLY: k_coarse<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
+      case M_RESID: k_coarse<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
+      case M_JACOBI: k_coarse<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
+      case M_DIAG: k_coarse<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
+      default: return fail(GMT_ERR_ARG, "bad mode");
+    }
+  }
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+template <int DPN>
+int launch_restrict(gmt_problem p, int l, const float* r, float* fc) {
+  const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
+  const Geo g = geo(bc.n, bc.nz);
+  Prof prof(p, l == 0 ? 3 : 4);
+  k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n);
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+template <int DPN>
+int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
+  const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
+  const Geo g = geo(bf.n, bf.nz);
+  Prof prof(p, l == 0 ? 2 : 4);
+  if (l == 0)
+    k_prolong_add<DPN, true><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
+                                                                 p->s, p->zm(0), nullptr);
+  else
+    k_prolong_add<DPN, false><<<g.grid, g.block, 0, p->stream>>>(
+        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0),
+        bf.S + (size_t)(13 * DPN * DPN) * bf.nodes);
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+template <int DPN>
+int smooth(gmt_problem p, int l, int sweeps) {
+  LevelBuf& b = p->lv[l];
+  const float* f = (l == 0) ? nullptr : b.f;
+  for (int it = 0; it < sweeps; ++it) {
+    const float* src = (it & 1) ? b.t : b.u;
+    float* dst = (it & 1) ? b.u : b.t;
+    TRY(launch_op<DPN>(p, l, M_JACOBI, src, f, dst, nullptr));
+  }
+  if (sweeps & 1)
+    CK(cudaMemcpyAsync(b.u, b.t, b.nodes * p->V * sizeof(float), cudaMemcpyDeviceToDevice, p->stream));
+  return GMT_OK;
+}
+
+template <int DPN>
+int coarsest(gmt_problem p) {
+  const int l = p->L - 1;
+  LevelBuf& b = p->lv[l];
+  const int sweeps = p->cfg.coarse_sweeps;
+  if (l == 0 || b.nodes > 32768) return smooth<DPN>(p, l, sweeps);
+  Prof prof(p, 5);
+  k_coarsest<DPN><<<1, 1024, 0, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps, (float)p->cfg.omega);
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+// Alg. 1 / Alg. 2: one V-cycle on the current level-0 solution.
+template <int DPN>
+int vcycle_once(gmt_problem p) {
+  const int L = p->L;
+  for (int l = 0; l < L - 1; ++l) {
+    LevelBuf& b = p->lv[l];
+    LevelBuf& c = p->lv[l + 1];
+    TRY(smooth<DPN>(p, l, p->cfg.pre_sweeps));                                  // pre-smoothing
+    TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? nullptr : b.f, b.r, nullptr));  // r = f - K u
+    TRY(launch_restrict<DPN>(p, l, b.r, c.f));                                   // f^{l+1} = R r^l
+    const size_t vb = c.nodes * p->V * sizeof(float);
+    if (c.inj_pending) CK(cudaMemcpyAsync(c.u, c.inj, vb, cudaMemcpyDeviceToDevice, p->stream));
+    else CK(cudaMemsetAsync(c.u, 0, vb, p->stream));                             // u^{l+1} = 0 / e_hat
+  }
+  TRY(coarsest<DPN>(p));                                                         // coarsest solve
+  for (int l = L - 2; l >= 0; --l) {
+    TRY(launch_prolong<DPN>(p, l, p->lv[l + 1].u, p->lv[l].u));                  // u += P u^{l+1}
+    TRY(smooth<DPN>(p, l, p->cfg.post_sweeps));                                  // post-smoothing
+  }
+  return GMT_OK;
+}
+
+int vcycle_dispatch(gmt_problem p) { return p->dpn == 3 ? vcycle_once<3>(p) : vcycle_once<1>(p); }
+
+// ---------------------------------------------------------------- setup
+
+template <int DPN>
+int build_operators(gmt_problem p) {
+  constexpr int ND = Tr<DPN>::ND;
+  cudaStream_t st = p->stream;
+  const int L = p->L;
+  if (L >= 2) {
+    LevelBuf& b = p->lv[1];
+    const Geo g = geo(b.n, b.nz);
+    Prof prof(p, 6);
+    k_stencil_l1<DPN><<<g.grid, g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, p->m1);
+    LAUNCHED(p);
+  }
+  for (int l = 2; l < L; ++l) {
+    LevelBuf& b = p->lv[l];
+    const unsigned nelem = (unsigned)b.nodes;
+    Prof prof(p, 6);
+    if (l == 2)
+      k_galerkin_elem<DPN, true><<<nelem, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M1g, b.Ke,
+                                                           b.n, b.nz, p->wc);
+    else
+      k_galerkin_elem<DPN, false><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, p->zm(l - 1), p->lv[l - 1].n,
+                                                            p->M1g, b.Ke, b.n, b.nz, p->wc);
+    LAUNCHED(p);
+    const Geo g = geo(b.n, b.nz);
+    k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz);
+    LAUNCHED(p);
+  }
+  return GMT_OK;
+}
+
+int upload_material(gmt_problem p, const void* material, int dtype, int location) {
+  const size_t nvox = (size_t)p->N * p->N * p->N;
+  if (!material) return fail(GMT_ERR_ARG, "material is NULL");
+  if (dtype == GMT_F32) {
+    CK(cudaMemcpyAsync(p->s, material, nvox * sizeof(float),
+                       location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, p->stream));
+  } else if (dtype == GMT_U8) {
+    const uint8_t* src = (const uint8_t*)material;
+    if (location == GMT_HOST) {
+      if (!p->u8tmp) TRY(dalloc(p, (void**)&p->u8tmp, nvox));
+      CK(cudaMemcpyAsync(p->u8tmp, material, nvox, cudaMemcpyHostToDevice, p->stream));
+      src = p->u8tmp;
+    }
+    k_u8_to_f32<<<1184, 256, 0, p->stream>>>(src, p->s, nvox);
+    LAUNCHED(p);
+  } else {
+    return fail(GMT_ERR_ARG, "unknown material dtype %d", dtype);
+  }
+  return GMT_OK;
+}
+
+int reset_solution(gmt_problem p) {
+  for (auto& b : p->lv) {
+    CK(cudaMemsetAsync(b.u, 0, b.nodes * p->V * sizeof(float), p->stream));
+    b.inj_pending = false;
+  }
+  return GMT_OK;
+}
+
+int rebuild(gmt_problem p) {
+  TRY(p->dpn == 3 ? build_operators<3>(p) : build_operators<1>(p));
+  TRY(reset_solution(p));
+  return GMT_OK;
+}
+
+int reduce(gmt_problem p, int nblk, int nv) {
+  k_reduce_partials<<<1, 256, 0, p->stream>>>(p->part, nblk, nv, p->red);
+  LAUNCHED(p);
+  CK(cudaMemcpyAsync(p->hred, p->red, nv * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return GMT_OK;
+}
+
+template <int DPN>
+int effective_tensor(gmt_problem p, const float* u, double* CH) {
+  constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
+  const LevelBuf& b = p->lv[0];
+  const Geo g = geo(b.n, b.nz);
+  {
+    Prof prof(p, 7);
+    k_effective_tensor<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, p->chc, p->part);
+    LAUNCHED(p);
+  }
+  TRY(reduce(p, g.nblk, NQ));
+  const double vol = (double)p->N * p->N * p->N;
+  int qi = 0;
+  for (int m = 0; m < NR; ++m)
+    for (int n = m; n < NR; ++n) {
+      const double v = p->hred[qi++] / vol;
+      CH[m * NR + n] = v;
+      CH[n * NR + m] = v;
+    }
+  return GMT_OK;
+}
+
+template <int DPN>
+int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
+  constexpr int NR = Tr<DPN>::NR;
+  LevelBuf& b = p->lv[0];
+  const Geo g = geo(b.n, b.nz);
+  TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part));
+  TRY(reduce(p, g.nblk, 2 * NR));
+  for (int m = 0; m < NR; ++m) {
+    const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[NR + m]);
+    if (rel) rel[m] = nf > 0 ? nr_ / nf : nr_;
+    if (ar) ar[m] = nr_;
+    if (af) af[m] = nf;
+  }
+  return GMT_OK;
+}
+
+template <int DPN>
+int zero_mean(gmt_problem p, float* dst) {
+  constexpr int V = Tr<DPN>::V;
+  const LevelBuf& b = p->lv[0];
+  const Geo g = geo(b.n, b.nz);
+  k_active_sum<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->part);
+  LAUNCHED(p);
+  k_reduce_partials<<<1, 256, 0, p->stream>>>(p->part, g.nblk, V + 1, p->red);
+  LAUNCHED(p);
+  k_sub_mean<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->red);
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+void drop_graph(gmt_problem p) {
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  p->gexec = nullptr;
+  p->graph_ok = false;
+  p->graph_pairs.clear();
+  for (cudaEvent_t e : p->gpool) cudaEventDestroy(e);
+  p->gpool.clear();
+}
+
+void free_all(gmt_problem p) {
+  drop_graph(p);
+  for (cudaEvent_t e : p->pool) cudaEventDestroy(e);
+  p->pool.clear();
+  for (auto& b : p->lv) {
+    cudaFree(b.u); cudaFree(b.t); cudaFree(b.f); cudaFree(b.r);
+    cudaFree(b.S); cudaFree(b.Ke); cudaFree(b.inj);
+  }
+  cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  if (p->hred) cudaFreeHost(p->hred);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+}
+
+int check_level(gmt_problem p, int level, bool allow_coarsest = true) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (level < 0 || level >= p->L || (!allow_coarsest && level >= p->L - 1))
+    return fail(GMT_ERR_ARG, "level %d out of range (L=%d)", level, p->L);
+  return GMT_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+
+extern "C" {
+
+int gmt_abi_version(void) { return GMT_ABI_VERSION; }
+const char* gmt_last_error(void) { return g_err.c_str(); }
+
+int gmt_default_config(gmt_config* cfg, int physics, int res) {
+  if (!cfg) return fail(GMT_ERR_ARG, "cfg is NULL");
+  if (physics != GMT_PHYSICS_ELASTIC && physics != GMT_PHYSICS_THERMAL)
+    return fail(GMT_ERR_ARG, "unknown physics %d", physics);
+  if (res < 2) return fail(GMT_ERR_ARG, "res must be >= 2");
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->physics = physics;
+  cfg->res = res;
+  cfg->levels = 0;
+  cfg->E = 1.0;
+  cfg->nu = 0.3;
+  cfg->kappa = 1.0;
+  cfg->omega = physics == GMT_PHYSICS_ELASTIC ? 0.45 : 0.6;
+  cfg->pre_sweeps = 2;
+  cfg->post_sweeps = 2;
+  cfg->coarse_sweeps = 16;
+  cfg->device = 0;
+  cfg->stream = nullptr;
+  cfg->use_graphs = 1;
+  return GMT_OK;
+}
+
+int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtype, int material_location,
+               gmt_problem* out) {
+  if (!cfg_in || !out) return fail(GMT_ERR_ARG, "null argument");
+  *out = nullptr;
+  gmt_config cfg = *cfg_in;
+  if (cfg.physics != GMT_PHYSICS_ELASTIC && cfg.physics != GMT_PHYSICS_THERMAL)
+    return fail(GMT_ERR_ARG, "unknown physics %d", cfg.physics);
+  if (cfg.res < 2) return fail(GMT_ERR_ARG, "res must be >= 2");
+  if (cfg.omega == 0.0) cfg.omega = cfg.physics == GMT_PHYSICS_ELASTIC ? 0.45 : 0.6;
+  if (!(cfg.omega > 0.0 && cfg.omega < 2.0)) return fail(GMT_ERR_ARG, "omega must be in (0, 2)");
+  if (cfg.pre_sweeps < 0 || cfg.post_sweeps < 0 || cfg.coarse_sweeps < 0)
+    return fail(GMT_ERR_ARG, "negative sweep count");
+  int L = cfg.levels;
+  if (L <= 0) {
+    L = 1;
+    int m = cfg.res;
+    while (m % 2 == 0 && m / 2 >= 4) { m /= 2; ++L; }
+  }
+  if (cfg.res % (1 << (L - 1)) != 0) return fail(GMT_ERR_ARG, "res %d not divisible by 2^(L-1)", cfg.res);
+  if ((cfg.res >> (L - 1)) < 2) return fail(GMT_ERR_ARG, "coarsest resolution must be >= 2");
+  cfg.levels = L;
+
+  gmt_problem p = new gmt_problem_s();
+  p->cfg = cfg;
+  p->N = cfg.res;
+  p->L = L;
+  if (!build_element_data(cfg.physics, cfg.E, cfg.nu, cfg.kappa, &p->ed)) {
+    delete p;
+    return fail(GMT_ERR_ARG, "invalid material constants (E>0, -1<nu<0.5, kappa>0)");
+  }
+  p->dpn = p->ed.dpn;
+  p->nr = p->ed.nrhs;
+  p->V = p->dpn * p->nr;
+  const int nd = p->ed.nd;
+  for (int i = 0; i < nd * nd; ++i) { p->fc.K[i] = (float)p->ed.K[i]; p->chc.K[i] = (float)p->ed.K[i]; }
+  for (int i = 0; i < nd * p->nr; ++i) { p->fc.F[i] = (float)p->ed.F[i]; p->chc.X0[i] = (float)p->ed.X0[i]; }
+  p->fc.omega = (float)cfg.omega;
+  for (int j = 0; j < 8; ++j)
+    for (int i = 0; i < nd * nd; ++i) p->m1.M[j * nd * nd + i] = (float)p->ed.M1[j][i];
+  for (int j = 0; j < 8; ++j)
+    for (int a = 0; a < 8; ++a)
+      for (int A = 0; A < 8; ++A) p->wc.W[(j * 8 + a) * 8 + A] = (float)p->ed.W[j][a][A];
+
+  int rc = GMT_OK;
+  auto bail = [&](int code) {
+    free_all(p);
+    delete p;
+    return code;
+  };
+  if ((rc = set_device(p)) != GMT_OK) return bail(rc);
+  if (cfg.stream) {
+    p->stream = (cudaStream_t)cfg.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(GMT_ERR_CUDA, "cudaStreamCreate failed"));
+    p->own_stream = true;
+  }
+  p->lv.resize(L);
+  const size_t V = p->V;
+  size_t max_blk = 0;
+  for (int l = 0; l < L; ++l) {
+    LevelBuf& b = p->lv[l];
+    b.n = cfg.res >> l;
+    b.nz = b.n;
+    b.nodes = (size_t)b.n * b.n * b.nz;
+    const size_t vb = b.nodes * V * sizeof(float);
+    if ((rc = dalloc(p, (void**)&b.u, vb)) || (rc = dalloc(p, (void**)&b.t, vb))) return bail(rc);
+    if (l >= 1 && (rc = dalloc(p, (void**)&b.f, vb))) return bail(rc);
+    if ((l < L - 1 || l == 0) && (rc = dalloc(p, (void**)&b.r, vb))) return bail(rc);
+    if (l >= 1 && (rc = dalloc(p, (void**)&b.S, b.nodes * 27 * p->dpn * p->dpn * sizeof(float)))) return bail(rc);
+    if (l >= 2 && (rc = dalloc(p, (void**)&b.Ke, b.nodes * nd * nd * sizeof(float)))) return bail(rc);
+    max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
+  }
+  p->part_cap = max_blk * 32;
+  if ((rc = dalloc(p, (void**)&p->part, p->part_cap * sizeof(double)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->red, 64 * sizeof(double)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->s, (size_t)p->N * p->N * p->N * sizeof(float)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);
+  if (cudaMallocHost(&p->hred, 64 * sizeof(double)) != cudaSuccess)
+    return bail(fail(GMT_ERR_NOMEM, "cudaMallocHost failed"));
+  if (cudaMemcpyAsync(p->M1g, p->m1.M, 8 * nd * nd * sizeof(float), cudaMemcpyHostToDevice, p->stream) !=
+      cudaSuccess)
+    return bail(fail(GMT_ERR_CUDA, "M1 upload failed"));
+  if ((rc = upload_material(p, material, material_dtype, material_location))) return bail(rc);
+  if ((rc = rebuild(p))) return bail(rc);
+  if (cudaStreamSynchronize(p->stream) != cudaSuccess) {
+    cudaError_t e = cudaGetLastError();
+    return bail(fail(GMT_ERR_CUDA, "setup failed: %s", cudaGetErrorString(e)));
+  }
+  *out = p;
+  return GMT_OK;
+}
+
+int gmt_set_material(gmt_problem p, const void* material, int dtype, int location) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  TRY(upload_material(p, material, dtype, location));
+  TRY(rebuild(p));
+  return GMT_OK;
+}
+
+int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  LevelBuf& b = p->lv[0];
+  const size_t vb = b.nodes * p->V * sizeof(float);
+  if (!u) CK(cudaMemsetAsync(b.u, 0, vb, p->stream));
+  else
+    CK(cudaMemcpyAsync(b.u, u, vb, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       p->stream));
+  return GMT_OK;
+}
+
+int gmt_inject_correction(gmt_problem p, int level, const float* e, int location) {
+  TRY(check_level(p, level));
+  if (level < 1) return fail(GMT_ERR_ARG, "injection level must be >= 1");
+  TRY(set_device(p));
+  LevelBuf& b = p->lv[level];
+  if (!e) { b.inj_pending = false; return GMT_OK; }
+  const size_t vb = b.nodes * p->V * sizeof(float);
+  if (!b.inj) TRY(dalloc(p, (void**)&b.inj, vb));
+  CK(cudaMemcpyAsync(b.inj, e, vb, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                     p->stream));
+  b.inj_pending = true;
+  return GMT_OK;
+}
+
+int gmt_vcycle(gmt_problem p, int ncycles) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (ncycles < 0) return fail(GMT_ERR_ARG, "ncycles < 0");
+  TRY(set_device(p));
+  for (int c = 0; c < ncycles; ++c) {
+    bool inj = false;
+    for (auto& b : p->lv) inj |= b.inj_pending;
+    if (inj || !p->cfg.use_graphs) {
+      TRY(vcycle_dispatch(p));
+      for (auto& b : p->lv) b.inj_pending = false;
+      continue;
+    }
+    if (!p->graph_ok) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+      p->capturing = true;
+      p->capture_count = 0;
+      int rc = vcycle_dispatch(p);
+      p->capturing = false;
+      cudaError_t ec = cudaStreamEndCapture(p->stream, &g);
+      p->graph_kernels = p->capture_count;
+      if (rc != GMT_OK) { if (g) cudaGraphDestroy(g); drop_graph(p); return rc; }
+      if (ec != cudaSuccess) return fail(GMT_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ec));
+      ec = cudaGraphInstantiate(&p->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (ec != cudaSuccess) return fail(GMT_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ec));
+      p->graph_ok = true;
+    }
+    CK(cudaGraphLaunch(p->gexec, p->stream));
+    p->launches += p->graph_kernels;
+    for (const auto& pr : p->graph_pairs) {
+      bool dup = false;
+      for (const auto& q : p->pending) dup |= (q.a == pr.a);
+      if (!dup) p->pending.push_back(pr);
+    }
+  }
+  return GMT_OK;
+}
+
+int gmt_profile_enable(gmt_problem p, unsigned mask) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  CK(cudaStreamSynchronize(p->stream));
+  drop_graph(p);
+  p->prof_mask = mask;
+  p->pending.clear();
+  for (int c = 0; c < 8; ++c) { p->prof_ms[c] = 0; p->prof_cnt[c] = 0; }
+  return GMT_OK;
+}
+
+int gmt_profile_collect(gmt_problem p) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  CK(cudaStreamSynchronize(p->stream));
+  for (const auto& pr : p->pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pr.a, pr.b));
+    if (pr.cls >= 0 && pr.cls < 8) { p->prof_ms[pr.cls] += ms; p->prof_cnt[pr.cls] += 1; }
+  }
+  p->pending.clear();
+  p->pool_next = 0;
+  return GMT_OK;
+}
+
+int gmt_profile_read(gmt_problem p, int cls, double* total_ms, long long* launches, int reset) {
+  if (!p || cls < 0 || cls >= 8) return fail(GMT_ERR_ARG, "bad profile class");
+  if (total_ms) *total_ms = p->prof_ms[cls];
+  if (launches) *launches = p->prof_cnt[cls];
+  if (reset) { p->prof_ms[cls] = 0; p->prof_cnt[cls] = 0; }
+  return GMT_OK;
+}
+
+long long gmt_kernel_launches(gmt_problem p) { return p ? p->launches : 0; }
+
+int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  return p->dpn == 3 ? residual_norms<3>(p, rel, abs_r, abs_f) : residual_norms<1>(p, rel, abs_r, abs_f);
+}
+
+int gmt_solve(gmt_problem p, double rel_tol, int max_cycles, int* cycles_done, double* final_rel,
+              double* history) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (max_cycles < 0) return fail(GMT_ERR_ARG, "max_cycles < 0");
+  double rel[6];
+  TRY(gmt_residual_norms(p, rel, nullptr, nullptr));
+  const int nr = p->nr;
+  auto worst = [&]() { double w = 0; for (int m = 0; m < nr; ++m) w = std::max(w, rel[m]); return w; };
+  if (history) for (int m = 0; m < nr; ++m) history[m] = rel[m];
+  int k = 0;
+  while (k < max_cycles && worst() > rel_tol) {
+    TRY(gmt_vcycle(p, 1));
+    ++k;
+    TRY(gmt_residual_norms(p, rel, nullptr, nullptr));
+    if (history) for (int m = 0; m < nr; ++m) history[k * nr + m] = rel[m];
+    if (!std::isfinite(worst())) break;
+  }
+  if (cycles_done) *cycles_done = k;
+  if (final_rel) *final_rel = worst();
+  return GMT_OK;
+}
+
+int gmt_homogenize(gmt_problem p, double* CH) {
+  if (!p || !CH) return fail(GMT_ERR_ARG, "null argument");
+  TRY(set_device(p));
+  return p->dpn == 3 ? effective_tensor<3>(p, p->lv[0].u, CH) : effective_tensor<1>(p, p->lv[0].u, CH);
+}
+
+int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) {
+  if (!p || !u) return fail(GMT_ERR_ARG, "null argument");
+  TRY(set_device(p));
+  LevelBuf& b = p->lv[0];
+  const size_t vb = b.nodes * p->V * sizeof(float);
+  float* dst = (location == GMT_DEVICE) ? u : b.r;   // r is scratch between cycles
+  CK(cudaMemcpyAsync(dst, b.u, vb, cudaMemcpyDeviceToDevice, p->stream));
+  if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
+  if (location == GMT_HOST) {
+    CK(cudaMemcpyAsync(u, dst, vb, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
+  return GMT_OK;
+}
+
+int gmt_num_levels(gmt_problem p) { return p ? p->L : GMT_ERR_ARG; }
+int gmt_level_res(gmt_problem p, int level) {
+  if (check_level(p, level) != GMT_OK) return GMT_ERR_ARG;
+  return p->lv[level].n;
+}
+int gmt_nrhs(gmt_problem p) { return p ? p->nr : GMT_ERR_ARG; }
+int gmt_dpn(gmt_problem p) { return p ? p->dpn : GMT_ERR_ARG; }
+void* gmt_stream(gmt_problem p) { return p ? (void*)p->stream : nullptr; }
+size_t gmt_device_bytes(gmt_problem p) { return p ? p->bytes : 0; }
+
+int gmt_sync(gmt_problem p) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(set_device(p));
+  CK(cudaStreamSynchronize(p->stream));
+  return GMT_OK;
+}
+
+void gmt_destroy(gmt_problem p) {
+  if (!p) return;
+  cudaSetDevice(p->cfg.device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  free_all(p);
+  delete p;
+}
+
+// ---- row-level entry points
+
+int gmt_op_apply(gmt_problem p, int level, const float* u, float* y) {
+  TRY(check_level(p, level));
+  if (!u || !y) return fail(GMT_ERR_ARG, "null vector");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_op<3>(p, level, M_APPLY, u, nullptr, y, nullptr)
+                     : launch_op<1>(p, level, M_APPLY, u, nullptr, y, nullptr);
+}
+
+int gmt_op_residual(gmt_problem p, int level, const float* u, const float* f, float* r) {
+  TRY(check_level(p, level));
+  if (!u || !r || (level > 0 && !f)) return fail(GMT_ERR_ARG, "null vector");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_op<3>(p, level, M_RESID, u, f, r, nullptr)
+                     : launch_op<1>(p, level, M_RESID, u, f, r, nullptr);
+}
+
+int gmt_op_jacobi(gmt_problem p, int level, const float* u, const float* f, float* u_out) {
+  TRY(check_level(p, level));
+  if (!u || !u_out || (level > 0 && !f)) return fail(GMT_ERR_ARG, "null vector");
+  if (u == u_out) return fail(GMT_ERR_ARG, "jacobi needs distinct in/out buffers");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_op<3>(p, level, M_JACOBI, u, f, u_out, nullptr)
+                     : launch_op<1>(p, level, M_JACOBI, u, f, u_out, nullptr);
+}
+
+int gmt_op_restrict(gmt_problem p, int level, const float* r, float* fc) {
+  TRY(check_level(p, level, false));
+  if (!r || !fc) return fail(GMT_ERR_ARG, "null vector");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_restrict<3>(p, level, r, fc) : launch_restrict<1>(p, level, r, fc);
+}
+
+int gmt_op_prolong_add(gmt_problem p, int level, const float* e, float* u) {
+  TRY(check_level(p, level, false));
+  if (!e || !u) return fail(GMT_ERR_ARG, "null vector");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_prolong<3>(p, level, e, u) : launch_prolong<1>(p, level, e, u);
+}
+
+int gmt_op_loads(gmt_problem p, float* f) {
+  if (!p || !f) return fail(GMT_ERR_ARG, "null argument");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_op<3>(p, 0, M_LOADS, p->lv[0].u, nullptr, f, nullptr)
+                     : launch_op<1>(p, 0, M_LOADS, p->lv[0].u, nullptr, f, nullptr);
+}
+
+int gmt_op_diagonal(gmt_problem p, int level, float* d) {
+  TRY(check_level(p, level));
+  if (!d) return fail(GMT_ERR_ARG, "null vector");
+  TRY(set_device(p));
+  return p->dpn == 3 ? launch_op<3>(p, level, M_DIAG, p->lv[level].u, nullptr, d, nullptr)
+                     : launch_op<1>(p, level, M_DIAG, p->lv[level].u, nullptr, d, nullptr);
+}
+
+int gmt_op_stencil(gmt_problem p, int level, float* S) {
+  TRY(check_level(p, level));
+  if (level < 1) return fail(GMT_ERR_ARG, "level 0 has no stored stencil (EBE from the material)");
+  if (!S) return fail(GMT_ERR_ARG, "null output");
+  TRY(set_device(p));
+  const LevelBuf& b = p->lv[level];
+  CK(cudaMemcpyAsync(S, b.S, b.nodes * 27 * p->dpn * p->dpn * sizeof(float), cudaMemcpyDeviceToDevice,
+                     p->stream));
+  return GMT_OK;
+}
+
+int gmt_op_effective_tensor(gmt_problem p, const float* u, double* CH) {
+  if (!p || !u || !CH) return fail(GMT_ERR_ARG, "null argument");
+  TRY(set_device(p));
+  return p->dpn == 3 ? effective_tensor<3>(p, u, CH) : effective_tensor<1>(p, u, CH);
+}
+
+}  // extern "C"

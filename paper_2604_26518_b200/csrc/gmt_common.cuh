@@ -1,0 +1,81 @@
+// Shared device-side definitions for libgmt kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gmt {
+
+// Per-physics compile-time shape: DPN dofs per node, NR load cases.
+template <int DPN> struct Tr {
+  static constexpr int NR = (DPN == 3) ? 6 : 3;  // App. F1: 6 strains / App. F2: 3 gradients
+  static constexpr int V = NR * DPN;             // floats per node in a vector
+  static constexpr int ND = 8 * DPN;             // element dofs
+  static constexpr int NS = 27 * DPN * DPN;      // stencil floats per node
+};
+
+// Plane addressing along z.  Single GPU: periodic wrap.  Slab-partitioned
+// (multi-GPU): planes -g..-1 and nz..nz+g-1 are ghost planes that live in
+// the same allocation, so indices are used as-is.
+struct ZMap {
+  int nz;
+  int wrap;
+  __device__ __forceinline__ int operator()(int p) const {
+    if (wrap) { if (p < 0) p += nz; else if (p >= nz) p -= nz; }
+    return p;
+  }
+};
+
+__device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+// Kernel parameter blocks: element constants live in the param constant bank,
+// so fully unrolled loops issue FFMA with c[0x0][imm] operands.
+struct FineConsts {      // level 0 (material-driven) operator
+  float K[24 * 24];      // unit-material element matrix
+  float F[24 * 6];       // element loads f_e (App. F1/F2)
+  float omega;
+};
+
+struct M1Consts {        // Galerkin child contributions P_j^T K P_j, 8 children
+  float M[8 * 24 * 24];
+};
+
+struct CHConsts {        // effective-tensor evaluation
+  float K[24 * 24];
+  float X0[24 * 6];
+};
+
+// Block-wide reduction of NV doubles per thread; thread 0 of the block
+// writes the NV block sums to out[0..NV).  Fixed summation order
+// (deterministic).  blockDim.x * blockDim.y * blockDim.z <= 1024.
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* __restrict__ out) {
+  __shared__ double sh[32][NV];
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double a = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0) sh[warp][k] = a;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (nthr + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double a = lane < nw ? sh[lane][k] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+      if (lane == 0) out[k] = a;
+    }
+  }
+}
+
+// Sum `nblk` rows of NV partials in a fixed order: out[k] = sum_b part[b*NV+k].
+__global__ void k_reduce_partials(const double* __restrict__ part, int nblk, int nv,
+                                  double* __restrict__ out);
+
+}  // namespace gmt

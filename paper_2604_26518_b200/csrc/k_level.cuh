@@ -1,0 +1,416 @@
+// Per-level hot-path kernels: EBE operator apply fused with residual / damped
+// Jacobi / loads / diagonal, full-weighting restriction, trilinear
+// prolongation + correction, and the single-CTA coarsest-level smoother.
+//
+// Thread mapping: one thread per node, 128-thread blocks tiling (x, y),
+// one z plane per blockIdx.z.  Nodal vectors are [z][y][x][m][c] float32
+// (V = NR*DPN floats per node, 72 B for elasticity), so the 27 neighbour
+// records a thread reads are contiguous 72 B runs shared through L1 with the
+// warp's other nodes.
+#pragma once
+
+#include "gmt_common.cuh"
+
+namespace gmt {
+
+enum Mode { M_APPLY = 0, M_RESID = 1, M_JACOBI = 2, M_LOADS = 3, M_DIAG = 4 };
+
+template <int DPN>
+__device__ __forceinline__ void load_node(const float* __restrict__ p, float (&v)[Tr<DPN>::V]) {
+  if constexpr (DPN == 3) {
+    const float2* q = reinterpret_cast<const float2*>(p);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const float2 t = __ldg(q + k);
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Tr<DPN>::V; ++k) v[k] = __ldg(p + k);
+  }
+}
+
+template <int DPN>
+__device__ __forceinline__ void store_node(float* __restrict__ p, const float (&v)[Tr<DPN>::V]) {
+  if constexpr (DPN == 3) {
+    float2* q = reinterpret_cast<float2*>(p);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) q[k] = make_float2(v[2 * k], v[2 * k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < Tr<DPN>::V; ++k) p[k] = v[k];
+  }
+}
+
+// Common epilogue of the operator kernels.  acc = (K u)_i, fl = f_i, D = diag.
+template <int DPN, int MODE>
+__device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp,
+                                            const float (&acc)[Tr<DPN>::V],
+                                            const float (&fl)[Tr<DPN>::V],
+                                            const float (&ui)[Tr<DPN>::V], const float (&D)[DPN],
+                                            float omega, double (&nrm)[2 * Tr<DPN>::NR]) {
+  constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
+  float o[V];
+#pragma unroll
+  for (int m = 0; m < NR; ++m)
+#pragma unroll
+    for (int p = 0; p < DPN; ++p) {
+      const int k = m * DPN + p;
+      const float r = fl[k] - acc[k];
+      if (MODE == M_APPLY) o[k] = acc[k];
+      else if (MODE == M_RESID) o[k] = r;
+      else if (MODE == M_LOADS) o[k] = fl[k];
+      else /* M_JACOBI */ o[k] = D[p] > 0.f ? fmaf(omega / D[p], r, ui[k]) : ui[k];
+      if (MODE == M_RESID || MODE == M_JACOBI) {
+        nrm[m] += valid ? (double)r * (double)r : 0.0;
+        nrm[NR + m] += valid ? (double)fl[k] * (double)fl[k] : 0.0;
+      }
+    }
+  if (valid) store_node<DPN>(outp, o);
+}
+
+// ---------------------------------------------------------------------------
+// Level 0: the EBE operator of Sec. 4.6 Eq. 14 evaluated from the material.
+// For every neighbour offset d in {-1,0,1}^3 the 27-point block
+//   A(d) = sum_{e containing i and i+d} s_e K_e[corner_e(i), corner_e(i+d)]
+// is formed in registers (shared by all NR load cases) and applied to u_{i+d}.
+// Loads f_i = sum_e s_e f_e[corner_e(i)] (Eq. 3) are formed the same way.
+// ---------------------------------------------------------------------------
+template <int DPN, int MODE>
+__global__ void __launch_bounds__(128)
+k_fine(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu,
+       const float* __restrict__ fext, float* __restrict__ out, int n, int nz,
+       const FineConsts P, double* __restrict__ part) {
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = T::V, ND = T::ND;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = blockIdx.z;
+  const bool valid = (x < n) && (y < n);
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  const ptrdiff_t node = z * plane + (ptrdiff_t)yc * n + xc;
+
+  float sc[8];
+  {
+    const int xs0 = wrapi(xc - 1, n), ys0 = wrapi(yc - 1, n), zs0 = zs(z - 1);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
+      const ptrdiff_t idx = (ez ? z : zs0) * plane + (ptrdiff_t)(ey ? yc : ys0) * n + (ex ? xc : xs0);
+      sc[e] = valid ? __ldg(s + idx) : 0.f;
+    }
+  }
+  bool act = false;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) act |= (sc[e] != 0.f);
+
+  float acc[V], fl[V], ui[V], D[DPN];
+#pragma unroll
+  for (int k = 0; k < V; ++k) { acc[k] = 0.f; fl[k] = 0.f; ui[k] = 0.f; }
+#pragma unroll
+  for (int p = 0; p < DPN; ++p) D[p] = 0.f;
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+
+  if (__any_sync(0xffffffffu, act)) {
+    if (MODE != M_LOADS) {
+#pragma unroll
+      for (int dz = -1; dz <= 1; ++dz) {
+        const ptrdiff_t zoff = (ptrdiff_t)zu(z + dz) * plane;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+          const ptrdiff_t yoff = zoff + (ptrdiff_t)wrapi(yc + dy, n) * n;
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            float A[DPN][DPN];
+#pragma unroll
+            for (int p = 0; p < DPN; ++p)
+#pragma unroll
+              for (int q = 0; q < DPN; ++q) A[p][q] = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
+              if ((dx == -1 && ex) || (dx == 1 && !ex) || (dy == -1 && ey) || (dy == 1 && !ey) ||
+                  (dz == -1 && ez) || (dz == 1 && !ez))
+                continue;
+              const int ki = (1 - ex) + 2 * (1 - ey) + 4 * (1 - ez);
+              const int kj = ki + dx + 2 * dy + 4 * dz;
+#pragma unroll
+              for (int p = 0; p < DPN; ++p)
+#pragma unroll
+                for (int q = 0; q < DPN; ++q)
+                  A[p][q] = fmaf(sc[e], P.K[(ki * DPN + p) * ND + kj * DPN + q], A[p][q]);
+            }
+            if (dx == 0 && dy == 0 && dz == 0) {
+#pragma unroll
+              for (int p = 0; p < DPN; ++p) D[p] = A[p][p];
+            }
+            if (MODE != M_DIAG) {
+              float uj[V];
+              load_node<DPN>(u + (yoff + wrapi(xc + dx, n)) * V, uj);
+              if (dx == 0 && dy == 0 && dz == 0) {
+#pragma unroll
+                for (int k = 0; k < V; ++k) ui[k] = uj[k];
+              }
+#pragma unroll
+              for (int m = 0; m < NR; ++m)
+#pragma unroll
+                for (int p = 0; p < DPN; ++p)
+#pragma unroll
+                  for (int q = 0; q < DPN; ++q)
+                    acc[m * DPN + p] = fmaf(A[p][q], uj[m * DPN + q], acc[m * DPN + p]);
+            }
+          }
+        }
+      }
+    }
+    if ((MODE == M_RESID || MODE == M_JACOBI || MODE == M_LOADS) && !fext) {
+      {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int ki = (1 - (e & 1)) + 2 * (1 - ((e >> 1) & 1)) + 4 * (1 - (e >> 2));
+#pragma unroll
+          for (int m = 0; m < NR; ++m)
+#pragma unroll
+            for (int p = 0; p < DPN; ++p)
+              fl[m * DPN + p] = fmaf(sc[e], P.F[(ki * DPN + p) * NR + m], fl[m * DPN + p]);
+        }
+      }
+    }
+  } else if (MODE == M_JACOBI) {
+    if (valid) load_node<DPN>(u + node * V, ui);   // whole warp inactive: copy through
+  }
+  if ((MODE == M_RESID || MODE == M_JACOBI) && fext && valid) load_node<DPN>(fext + node * V, fl);
+
+  if (MODE == M_DIAG) {
+    if (valid) {
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) out[node * DPN + p] = D[p];
+    }
+  } else {
+    op_epilogue<DPN, MODE>(valid, out + node * V, acc, fl, ui, D, P.omega, nrm);
+  }
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Levels >= 1: the Galerkin operator stored as a 27-point block stencil in
+// SoA layout S[((d*DPN + p)*DPN + q) * nodes + node] (coalesced over x).
+// ---------------------------------------------------------------------------
+template <int DPN, int MODE>
+__global__ void __launch_bounds__(128)
+k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
+         const float* __restrict__ f, float* __restrict__ out, int n, int nz, float omega,
+         double* __restrict__ part) {
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = T::V;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = blockIdx.z;
+  const bool valid = (x < n) && (y < n);
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  const ptrdiff_t nodes = plane * nz;
+  const ptrdiff_t node = z * plane + (ptrdiff_t)yc * n + xc;
+
+  float D[DPN];
+#pragma unroll
+  for (int p = 0; p < DPN; ++p) D[p] = valid ? __ldg(S + ((13 * DPN + p) * DPN + p) * nodes + node) : 0.f;
+  bool act = false;
+#pragma unroll
+  for (int p = 0; p < DPN; ++p) act |= (D[p] != 0.f);
+
+  float acc[V], fl[V], ui[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) { acc[k] = 0.f; fl[k] = 0.f; ui[k] = 0.f; }
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+
+  if (__any_sync(0xffffffffu, act)) {
+    if (MODE != M_DIAG && MODE != M_LOADS) {
+#pragma unroll
+      for (int d = 0; d < 27; ++d) {
+        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+        float A[DPN][DPN];
+#pragma unroll
+        for (int p = 0; p < DPN; ++p)
+#pragma unroll
+          for (int q = 0; q < DPN; ++q)
+            A[p][q] = valid ? __ldg(S + ((d * DPN + p) * DPN + q) * nodes + node) : 0.f;
+        float uj[V];
+        load_node<DPN>(u + ((ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(yc + dy, n) * n +
+                            wrapi(xc + dx, n)) * V, uj);
+        if (d == 13) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) ui[k] = uj[k];
+        }
+#pragma unroll
+        for (int m = 0; m < NR; ++m)
+#pragma unroll
+          for (int p = 0; p < DPN; ++p)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q)
+              acc[m * DPN + p] = fmaf(A[p][q], uj[m * DPN + q], acc[m * DPN + p]);
+      }
+    }
+  } else if (MODE == M_JACOBI) {
+    if (valid) load_node<DPN>(u + node * V, ui);
+  }
+  if ((MODE == M_RESID || MODE == M_JACOBI) && valid) load_node<DPN>(f + node * V, fl);
+  if (MODE == M_DIAG) {
+    if (valid) {
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) out[node * DPN + p] = D[p];
+    }
+  } else {
+    op_epilogue<DPN, MODE>(valid, out + node * V, acc, fl, ui, D, omega, nrm);
+  }
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// App. E2 restriction R = P^T in gather form: coarse node I collects the 27
+// fine nodes 2I + delta with the full-weighting weights prod_d (1 - |delta_d|/2).
+// ---------------------------------------------------------------------------
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc, int nzc, int nf) {
+  constexpr int V = Tr<DPN>::V;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z = blockIdx.z;
+  if (X >= nc || Y >= nc) return;
+  const ptrdiff_t pf = (ptrdiff_t)nf * nf;
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const float w = (dx ? 0.5f : 1.f) * (dy ? 0.5f : 1.f) * (dz ? 0.5f : 1.f);
+        const ptrdiff_t i = (ptrdiff_t)zf(2 * Z + dz) * pf + (ptrdiff_t)wrapi(2 * Y + dy, nf) * nf +
+                            wrapi(2 * X + dx, nf);
+        float v[V];
+        load_node<DPN>(r + i * V, v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = fmaf(w, v[k], acc[k]);
+      }
+  store_node<DPN>(fc + ((ptrdiff_t)Z * nc * nc + (ptrdiff_t)Y * nc + X) * V, acc);
+}
+
+// ---------------------------------------------------------------------------
+// App. E2 prolongation as a weighted gather, fused with the correction
+// u^l += P u^{l+1} (Alg. 1 line 10), on active fine nodes only (App. E2: the
+// stencil exists "for each active fine node").  Activity: level 0 -> any of
+// the 8 incident voxels non-void; level >= 1 -> nonzero stencil diagonal.
+// ---------------------------------------------------------------------------
+template <int DPN, bool FINE0>
+__global__ void __launch_bounds__(128)
+k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int nf, int nzf, int nc,
+              const float* __restrict__ s, ZMap zs, const float* __restrict__ Sdiag) {
+  constexpr int V = Tr<DPN>::V;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = blockIdx.z;
+  if (x >= nf || y >= nf) return;
+  const ptrdiff_t pf = (ptrdiff_t)nf * nf;
+  const ptrdiff_t node = z * pf + (ptrdiff_t)y * nf + x;
+  bool act = false;
+  if (FINE0) {
+    const int xs0 = wrapi(x - 1, nf), ys0 = wrapi(y - 1, nf), zs0 = zs(z - 1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const ptrdiff_t idx = ((k >> 2) ? z : zs0) * pf + (ptrdiff_t)(((k >> 1) & 1) ? y : ys0) * nf +
+                            ((k & 1) ? x : xs0);
+      act |= (__ldg(s + idx) != 0.f);
+    }
+  } else {
+    act = __ldg(Sdiag + node) != 0.f;
+  }
+  if (!act) return;
+  const int X0 = x >> 1, Y0 = y >> 1, Z0 = z >> 1;
+  const int rx = x & 1, ry = y & 1, rz = z & 1;
+  const int X1 = wrapi(X0 + 1, nc), Y1 = wrapi(Y0 + 1, nc), Z1 = zc(Z0 + 1);
+  const ptrdiff_t pc = (ptrdiff_t)nc * nc;
+  float acc[V];
+  load_node<DPN>(u + node * V, acc);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+    if ((ox && !rx) || (oy && !ry) || (oz && !rz)) continue;
+    const float w = (rx ? 0.5f : 1.f) * (ry ? 0.5f : 1.f) * (rz ? 0.5f : 1.f);
+    const ptrdiff_t ic = (ptrdiff_t)(oz ? Z1 : Z0) * pc + (ptrdiff_t)(oy ? Y1 : Y0) * nc + (ox ? X1 : X0);
+    float v[V];
+    load_node<DPN>(e + ic * V, v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = fmaf(w, v[k], acc[k]);
+  }
+  store_node<DPN>(u + node * V, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Coarsest level (Alg. 1 line 8): `sweeps` damped-Jacobi sweeps inside one
+// CTA (the whole coarsest grid, periodic in all axes), ping-ponging u <-> t
+// through L1/L2 with a block barrier between sweeps.  Result ends in u.
+// ---------------------------------------------------------------------------
+template <int DPN>
+__global__ void __launch_bounds__(1024)
+k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, float* t, int n,
+           int sweeps, float omega) {
+  constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
+  const int nodes = n * n * n;
+  for (int it = 0; it < sweeps; ++it) {
+    const float* src = (it & 1) ? t : u;
+    float* dst = (it & 1) ? u : t;
+    for (int i = threadIdx.x; i < nodes; i += blockDim.x) {
+      const int x = i % n, y = (i / n) % n, z = i / (n * n);
+      float acc[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] = 0.f;
+      for (int d = 0; d < 27; ++d) {
+        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+        const int j = (wrapi(z + dz, n) * n + wrapi(y + dy, n)) * n + wrapi(x + dx, n);
+        float A[DPN][DPN];
+#pragma unroll
+        for (int p = 0; p < DPN; ++p)
+#pragma unroll
+          for (int q = 0; q < DPN; ++q) A[p][q] = S[((d * DPN + p) * DPN + q) * nodes + i];
+#pragma unroll
+        for (int m = 0; m < NR; ++m)
+#pragma unroll
+          for (int p = 0; p < DPN; ++p)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q)
+              acc[m * DPN + p] = fmaf(A[p][q], src[j * V + m * DPN + q], acc[m * DPN + p]);
+      }
+#pragma unroll
+      for (int m = 0; m < NR; ++m)
+#pragma unroll
+        for (int p = 0; p < DPN; ++p) {
+          const int k = m * DPN + p;
+          const float Dp = S[((13 * DPN + p) * DPN + p) * nodes + i];
+          const float ui = src[i * V + k];
+          dst[i * V + k] = Dp > 0.f ? fmaf(omega / Dp, f[i * V + k] - acc[k], ui) : ui;
+        }
+    }
+    __syncthreads();
+  }
+  if (sweeps & 1) {
+    for (int i = threadIdx.x; i < nodes * V; i += blockDim.x) u[i] = t[i];
+  }
+}
+
+}  // namespace gmt

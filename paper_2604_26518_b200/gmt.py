@@ -1,0 +1,301 @@
+"""Thin ctypes binding over libgmt (include/gmt.h).  Argument marshalling only:
+every step of the path runs in libgmt's CUDA kernels.  There is no CPU
+fallback -- loading fails loudly when libgmt.so is missing.
+
+Arrays: numpy arrays are passed as host buffers (GMT_HOST); torch CUDA
+tensors as device buffers (GMT_DEVICE).  Nodal vectors are float32
+[z, y, x, m, c] (m = load case, c = component); material fields float32
+or uint8 [z, y, x].
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgmt.so")
+
+GMT_OK = 0
+PHYSICS = {"elastic": 0, "thermal": 1}
+GMT_F32, GMT_U8 = 0, 1
+GMT_HOST, GMT_DEVICE = 0, 1
+
+
+class GmtError(RuntimeError):
+    pass
+
+
+class gmt_config(C.Structure):
+    _fields_ = [
+        ("physics", C.c_int), ("res", C.c_int), ("levels", C.c_int),
+        ("E", C.c_double), ("nu", C.c_double), ("kappa", C.c_double), ("omega", C.c_double),
+        ("pre_sweeps", C.c_int), ("post_sweeps", C.c_int), ("coarse_sweeps", C.c_int),
+        ("device", C.c_int), ("stream", C.c_void_p), ("use_graphs", C.c_int),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/gmt.h
+_P = C.c_void_p
+_FP = C.c_void_p
+_DP = C.POINTER(C.c_double)
+SIGNATURES = {
+    "gmt_default_config": (C.c_int, [C.POINTER(gmt_config), C.c_int, C.c_int]),
+    "gmt_create": (C.c_int, [C.POINTER(gmt_config), C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "gmt_set_material": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int]),
+    "gmt_set_initial_guess": (C.c_int, [_P, _FP, C.c_int]),
+    "gmt_inject_correction": (C.c_int, [_P, C.c_int, _FP, C.c_int]),
+    "gmt_vcycle": (C.c_int, [_P, C.c_int]),
+    "gmt_residual_norms": (C.c_int, [_P, _DP, _DP, _DP]),
+    "gmt_solve": (C.c_int, [_P, C.c_double, C.c_int, C.POINTER(C.c_int), _DP, _DP]),
+    "gmt_homogenize": (C.c_int, [_P, _DP]),
+    "gmt_get_solution": (C.c_int, [_P, _FP, C.c_int, C.c_int]),
+    "gmt_num_levels": (C.c_int, [_P]),
+    "gmt_level_res": (C.c_int, [_P, C.c_int]),
+    "gmt_nrhs": (C.c_int, [_P]),
+    "gmt_dpn": (C.c_int, [_P]),
+    "gmt_stream": (C.c_void_p, [_P]),
+    "gmt_device_bytes": (C.c_size_t, [_P]),
+    "gmt_sync": (C.c_int, [_P]),
+    "gmt_destroy": (None, [_P]),
+    "gmt_last_error": (C.c_char_p, []),
+    "gmt_abi_version": (C.c_int, []),
+    "gmt_profile_enable": (C.c_int, [_P, C.c_uint]),
+    "gmt_profile_collect": (C.c_int, [_P]),
+    "gmt_profile_read": (C.c_int, [_P, C.c_int, _DP, C.POINTER(C.c_longlong), C.c_int]),
+    "gmt_kernel_launches": (C.c_longlong, [_P]),
+    "gmt_op_apply": (C.c_int, [_P, C.c_int, _FP, _FP]),
+    "gmt_op_residual": (C.c_int, [_P, C.c_int, _FP, _FP, _FP]),
+    "gmt_op_jacobi": (C.c_int, [_P, C.c_int, _FP, _FP, _FP]),
+    "gmt_op_restrict": (C.c_int, [_P, C.c_int, _FP, _FP]),
+    "gmt_op_prolong_add": (C.c_int, [_P, C.c_int, _FP, _FP]),
+    "gmt_op_loads": (C.c_int, [_P, _FP]),
+    "gmt_op_diagonal": (C.c_int, [_P, C.c_int, _FP]),
+    "gmt_op_stencil": (C.c_int, [_P, C.c_int, _FP]),
+    "gmt_op_effective_tensor": (C.c_int, [_P, _FP, _DP]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgmt.so (raises GmtError if it is missing -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise GmtError(f"libgmt.so not built at {path}; run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.gmt_abi_version() != 1:
+        raise GmtError("libgmt ABI mismatch")
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != GMT_OK:
+        raise GmtError(f"{what} failed ({rc}): {_lib.gmt_last_error().decode()}")
+
+
+def _buf(a, dtype=None, writable=False):
+    """(pointer, location) of a numpy array (host) or torch CUDA tensor (device)."""
+    if a is None:
+        return None, GMT_HOST
+    if isinstance(a, np.ndarray):
+        if dtype is not None and a.dtype != dtype:
+            raise TypeError(f"expected {dtype}, got {a.dtype}")
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, GMT_HOST
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if not a.is_cuda:
+            raise ValueError("torch tensors must be CUDA tensors (use numpy for host buffers)")
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if dtype is not None and a.dtype != {np.float32: torch.float32, np.uint8: torch.uint8}[dtype]:
+            raise TypeError(f"expected {dtype}, got {a.dtype}")
+        return a.data_ptr(), GMT_DEVICE
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+def _dptr(a):
+    p, loc = _buf(a, np.float32)
+    if loc != GMT_DEVICE:
+        raise ValueError("row-level ops take torch CUDA tensors")
+    return p
+
+
+class Problem:
+    """One periodic cell problem set (all load cases) on one GPU: gmt_create."""
+
+    def __init__(self, material, physics: str = "elastic", levels: int = 0, E: float = 1.0,
+                 nu: float = 0.3, kappa: float = 1.0, omega: float = 0.0, pre_sweeps: int = 2,
+                 post_sweeps: int = 2, coarse_sweeps: int = 16, device: int = 0, stream=None,
+                 use_graphs: bool = True):
+        lib = load()
+        n = int(material.shape[0])
+        if tuple(material.shape) != (n, n, n):
+            raise ValueError("material must be (N, N, N)")
+        cfg = gmt_config()
+        _check(lib.gmt_default_config(C.byref(cfg), PHYSICS[physics], n), "gmt_default_config")
+        cfg.levels, cfg.E, cfg.nu, cfg.kappa, cfg.omega = levels, E, nu, kappa, omega
+        cfg.pre_sweeps, cfg.post_sweeps, cfg.coarse_sweeps = pre_sweeps, post_sweeps, coarse_sweeps
+        cfg.device = device
+        cfg.stream = stream
+        cfg.use_graphs = int(use_graphs)
+        ptr, loc, dt = self._material(material)
+        h = C.c_void_p()
+        _check(lib.gmt_create(C.byref(cfg), ptr, dt, loc, C.byref(h)), "gmt_create")
+        self._h = h
+        self.lib = lib
+        self.physics = physics
+        self.n = n
+        self.levels = lib.gmt_num_levels(h)
+        self.nrhs = lib.gmt_nrhs(h)
+        self.dpn = lib.gmt_dpn(h)
+
+    @staticmethod
+    def _material(material):
+        dt = GMT_U8 if str(material.dtype) in ("uint8", "torch.uint8") else GMT_F32
+        ptr, loc = _buf(material, np.uint8 if dt == GMT_U8 else np.float32)
+        return ptr, loc, dt
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.gmt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- shape helpers -----------------------------------------------------
+    def level_res(self, level: int) -> int:
+        return self.lib.gmt_level_res(self._h, level)
+
+    def vec_shape(self, level: int = 0):
+        n = self.level_res(level)
+        return (n, n, n, self.nrhs, self.dpn)
+
+    @property
+    def stream(self) -> int:
+        return self.lib.gmt_stream(self._h)
+
+    @property
+    def device_bytes(self) -> int:
+        return self.lib.gmt_device_bytes(self._h)
+
+    # -- the boundary --------------------------------------------------------
+    def gmt_set_material(self, material):
+        ptr, loc, dt = self._material(material)
+        _check(self.lib.gmt_set_material(self._h, ptr, dt, loc), "gmt_set_material")
+
+    def gmt_set_initial_guess(self, u=None):
+        ptr, loc = _buf(u, np.float32)
+        _check(self.lib.gmt_set_initial_guess(self._h, ptr, loc), "gmt_set_initial_guess")
+
+    def gmt_inject_correction(self, level: int, e=None):
+        ptr, loc = _buf(e, np.float32)
+        _check(self.lib.gmt_inject_correction(self._h, level, ptr, loc), "gmt_inject_correction")
+
+    def gmt_vcycle(self, ncycles: int = 1):
+        _check(self.lib.gmt_vcycle(self._h, ncycles), "gmt_vcycle")
+
+    def gmt_residual_norms(self):
+        rel = (C.c_double * self.nrhs)()
+        ar = (C.c_double * self.nrhs)()
+        af = (C.c_double * self.nrhs)()
+        _check(self.lib.gmt_residual_norms(self._h, rel, ar, af), "gmt_residual_norms")
+        return np.array(rel), np.array(ar), np.array(af)
+
+    def gmt_solve(self, rel_tol: float = 1e-5, max_cycles: int = 100):
+        hist = (C.c_double * ((max_cycles + 1) * self.nrhs))()
+        k = C.c_int()
+        fr = C.c_double()
+        _check(self.lib.gmt_solve(self._h, rel_tol, max_cycles, C.byref(k), C.byref(fr), hist), "gmt_solve")
+        h = np.array(hist).reshape(max_cycles + 1, self.nrhs)[: k.value + 1]
+        return k.value, fr.value, h
+
+    def gmt_homogenize(self):
+        CH = (C.c_double * (self.nrhs * self.nrhs))()
+        _check(self.lib.gmt_homogenize(self._h, CH), "gmt_homogenize")
+        return np.array(CH).reshape(self.nrhs, self.nrhs)
+
+    def gmt_get_solution(self, out=None, zero_mean: bool = False):
+        if out is None:
+            out = np.empty(self.vec_shape(0), dtype=np.float32)
+        ptr, loc = _buf(out, np.float32)
+        _check(self.lib.gmt_get_solution(self._h, ptr, loc, int(zero_mean)), "gmt_get_solution")
+        return out
+
+    def gmt_sync(self):
+        _check(self.lib.gmt_sync(self._h), "gmt_sync")
+
+    # -- live profiling ------------------------------------------------------
+    PROFILE_CLASSES = ("l0_jacobi", "l0_residual", "l0_prolong", "restrict01", "coarse_levels",
+                       "coarsest", "galerkin_setup", "effective_tensor")
+
+    def gmt_profile_enable(self, mask: int):
+        _check(self.lib.gmt_profile_enable(self._h, mask), "gmt_profile_enable")
+
+    def gmt_profile_collect(self):
+        _check(self.lib.gmt_profile_collect(self._h), "gmt_profile_collect")
+
+    def gmt_profile_read(self, cls: int, reset: bool = False):
+        ms = C.c_double()
+        cnt = C.c_longlong()
+        _check(self.lib.gmt_profile_read(self._h, cls, C.byref(ms), C.byref(cnt), int(reset)), "gmt_profile_read")
+        return ms.value, cnt.value
+
+    def gmt_kernel_launches(self) -> int:
+        return self.lib.gmt_kernel_launches(self._h)
+
+    # -- row-level entry points (torch CUDA tensors) -------------------------
+    def gmt_op_apply(self, level, u, y):
+        _check(self.lib.gmt_op_apply(self._h, level, _dptr(u), _dptr(y)), "gmt_op_apply")
+
+    def gmt_op_residual(self, level, u, f, r):
+        fp = None if f is None else _dptr(f)
+        _check(self.lib.gmt_op_residual(self._h, level, _dptr(u), fp, _dptr(r)), "gmt_op_residual")
+
+    def gmt_op_jacobi(self, level, u, f, u_out):
+        fp = None if f is None else _dptr(f)
+        _check(self.lib.gmt_op_jacobi(self._h, level, _dptr(u), fp, _dptr(u_out)), "gmt_op_jacobi")
+
+    def gmt_op_restrict(self, level, r, fc):
+        _check(self.lib.gmt_op_restrict(self._h, level, _dptr(r), _dptr(fc)), "gmt_op_restrict")
+
+    def gmt_op_prolong_add(self, level, e, u):
+        _check(self.lib.gmt_op_prolong_add(self._h, level, _dptr(e), _dptr(u)), "gmt_op_prolong_add")
+
+    def gmt_op_loads(self, f):
+        _check(self.lib.gmt_op_loads(self._h, _dptr(f)), "gmt_op_loads")
+
+    def gmt_op_diagonal(self, level, d):
+        _check(self.lib.gmt_op_diagonal(self._h, level, _dptr(d)), "gmt_op_diagonal")
+
+    def gmt_op_stencil(self, level, S):
+        _check(self.lib.gmt_op_stencil(self._h, level, _dptr(S)), "gmt_op_stencil")
+
+    def gmt_op_effective_tensor(self, u):
+        CH = (C.c_double * (self.nrhs * self.nrhs))()
+        _check(self.lib.gmt_op_effective_tensor(self._h, _dptr(u), CH), "gmt_op_effective_tensor")
+        return np.array(CH).reshape(self.nrhs, self.nrhs)

@@ -154,7 +154,7 @@ def stochastic(n: int, vf: float = 0.3, seed: int = 0, corr: float = 0.08,
     kz, ky, kx = k[:, None, None], k[None, :, None], k[None, None, :]
     k2 = (kx * kx + ky * ky + kz * kz).astype(np.float32)
     filt = np.exp(-0.5 * (_TWO_PI * corr) ** 2 * k2).astype(np.float32)
-    g = np.fft.irfftn(np.fft.rfftn(w) * filt[:, :, : n // 2 + 1], s=(n, n, n)).astype(np.float32)
+    g = np.fft.irfftn(np.fft.rfftn(w) * filt[:, :, : n // 2 + 1], s=(n, n, n), axes=(0, 1, 2)).astype(np.float32)
     if sheet:
         g = np.abs(g)
     return _threshold_to_vf(g, vf, below=True)
