@@ -19,8 +19,10 @@
  *    scale it (App. F3 Eq. C_e = (rho_min + rho^p) C_0 evaluated by the
  *    caller).  GMT_U8 input is occupancy: byte != 0 -> s = 1.
  *  - Nodal vectors at level l (resolution n_l = N / 2^l, l = 0 finest):
- *    float32 [z][y][x][m][c], m = load case (6 elastic / 3 thermal),
- *    c = component (3 / 1); n_l^3 * NRHS * DPN floats, contiguous.
+ *    float32 component planes [m][c][z][y][x], m = load case (6 elastic /
+ *    3 thermal), c = component (3 / 1); NRHS * DPN * n_l^3 floats,
+ *    contiguous (value (m,c) of node i at index (m*DPN + c) * n_l^3 + i,
+ *    node i = x + n_l (y + n_l z)).
  *  - Voigt order (11,22,33,23,13,12), engineering shear.
  *  - Inactive nodes (every incident voxel void) are outside the active set
  *    (Sec. 4.1.1): smoothing and prolongation leave them untouched.
@@ -192,7 +194,7 @@ GMT_API int gmt_op_restrict(gmt_problem p, int level, const float* r, float* fc)
 GMT_API int gmt_op_prolong_add(gmt_problem p, int level, const float* e, float* u);
 /* Eq. 3 load vector f = sum_e A_e^T s_e f_e at level 0. */
 GMT_API int gmt_op_loads(gmt_problem p, float* f);
-/* diag(K^l), layout [z][y][x][c] (n_l^3 * DPN floats). */
+/* diag(K^l), layout [c][z][y][x] (DPN * n_l^3 floats). */
 GMT_API int gmt_op_diagonal(gmt_problem p, int level, float* d);
 /* The assembled Galerkin operator of level l >= 1 as a 27-point block
  * stencil: S[((d*DPN + a)*DPN + b) * n_l^3 + node], d = (dx+1) + 3(dy+1) +

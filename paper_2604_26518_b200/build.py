@@ -33,7 +33,7 @@ def _deps():
     out = []
     for d in (CSRC, os.path.join(ROOT, "include")):
         for f in sorted(os.listdir(d)):
-            if f.endswith((".cu", ".cuh", ".h", ".cpp")):
+            if f.endswith((".cu", ".cuh", ".h", ".cpp", ".inc")):
                 out.append(os.path.join(d, f))
     return out
 
@@ -45,7 +45,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
+TABLES = os.path.join(CSRC, "gmt_tables.inc")
+
+
+def gen_tables(verbose: bool = False):
+    """Compile and run gen_tables.cpp (host) -> csrc/gmt_tables.inc."""
+    exe = os.path.join(CSRC, ".gen_tables")
+    cxx = shutil.which("g++") or shutil.which("c++")
+    cmd = [cxx, "-O1", "-std=c++17", "-o", exe, os.path.join(CSRC, "gen_tables.cpp"),
+           os.path.join(CSRC, "gmt_fem.cpp")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gen_tables build failed:\n{res.stderr}")
+    res = subprocess.run([exe, TABLES + ".tmp"], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("gen_tables failed")
+    os.replace(TABLES + ".tmp", TABLES)
+    os.remove(exe)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    if force or not os.path.exists(TABLES) or \
+            os.path.getmtime(TABLES) < max(os.path.getmtime(os.path.join(CSRC, f))
+                                           for f in ("gen_tables.cpp", "gmt_fem.cpp", "gmt_fem.h")):
+        gen_tables(verbose)
     if not force and up_to_date():
         return LIB
     cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]

@@ -3,16 +3,21 @@
 // included here so every template is instantiated next to its launcher.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/gmt.h"
 #include "gmt_fem.h"
+#include "k_fine_tiled.cuh"
 #include "k_level.cuh"
 #include "k_reduce.cuh"
 #include "k_setup.cuh"
@@ -85,15 +90,23 @@ struct gmt_problem_s {
   std::vector<LevelBuf> lv;
   ElementData ed{};
   FineConsts fc{};
-  M1Consts m1{};
-  CHConsts chc{};
+
   WConsts wc{};
   float* M1g = nullptr;
+  float* M2g = nullptr;
   double* part = nullptr;
   size_t part_cap = 0;   // doubles
   double* red = nullptr; // device reduction results
   double* hred = nullptr;  // pinned host mirror
   uint8_t* u8tmp = nullptr;
+  uint8_t* tflag = nullptr;   // level-0 tile activity flags (k_tile_flags)
+  uint8_t* iflag = nullptr;   // level-0 interface-node flags (k_iface_flags)
+  int* ilist = nullptr;       // sorted interface-node list (static per material)
+  int* icount_d = nullptr;
+  int icount = 0;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int tntx = 0, tnty = 0;
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
@@ -131,6 +144,8 @@ int set_device(gmt_problem p) {
   CK(cudaSetDevice(p->cfg.device));
   return GMT_OK;
 }
+
+void drop_graph(gmt_problem p);
 
 // ---------------------------------------------------------------- accounting
 
@@ -181,29 +196,55 @@ struct Prof {
 // ---------------------------------------------------------------- launches
 
 template <int DPN>
-int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part) {
+int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part,
+              int skip_void = 0) {
   const LevelBuf& b = p->lv[l];
   const Geo g = geo(b.n, b.nz);
   cudaStream_t st = p->stream;
   const float om = (float)p->cfg.omega;
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
-  if (l == 0) {
+  const ptrdiff_t cs = (ptrdiff_t)b.nodes;
+  if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
+    const ZMap z = p->zm(0);
+    const dim3 grid(p->tntx, p->tnty, (b.nz + TT_ZC - 1) / TT_ZC), block(TT_X, TT_Y);
+    const size_t shm = (size_t)TT_NB * Tr<DPN>::V * TT_PLS * sizeof(float);
+    const int nbt = grid.x * grid.y * grid.z;
+    double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
+    const int nbi = (p->icount + 127) / 128;
+    if (mode == M_JACOBI)
+      k_fine_tiled<DPN, M_JACOBI><<<grid, block, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                            p->tflag, p->tntx, p->tnty);
+    else
+      k_fine_tiled<DPN, M_RESID><<<grid, block, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                           p->tflag, p->tntx, p->tnty);
+    LAUNCHED(p);
+    if (nbi > 0) {
+      if (mode == M_JACOBI)
+        k_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
+                                                    p->icount);
+      else
+        k_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
+                                                   p->icount);
+    } else {
+      return GMT_OK;
+    }
+  } else if (l == 0) {
     const ZMap z = p->zm(0);
     switch (mode) {
-      case M_APPLY: k_fine<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
-      case M_RESID: k_fine<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
-      case M_JACOBI: k_fine<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
-      case M_LOADS: k_fine<DPN, M_LOADS><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
-      case M_DIAG: k_fine<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part); break;
+      case M_APPLY: k_fine<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
+      case M_RESID: k_fine<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
+      case M_JACOBI: k_fine<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
+      case M_LOADS: k_fine<DPN, M_LOADS><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
+      case M_DIAG: k_fine<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
       default: return fail(GMT_ERR_ARG, "bad mode");
     }
   } else {
     const ZMap z = p->zm(l);
     switch (mode) {
-      case M_APPLY: k_coarse<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
-      case M_RESID: k_coarse<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
-      case M_JACOBI: k_coarse<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
-      case M_DIAG: k_coarse<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part); break;
+      case M_APPLY: k_coarse<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
+      case M_RESID: k_coarse<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
+      case M_JACOBI: k_coarse<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
+      case M_DIAG: k_coarse<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
       default: return fail(GMT_ERR_ARG, "bad mode");
     }
   }
@@ -212,11 +253,13 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
 }
 
 template <int DPN>
-int launch_restrict(gmt_problem p, int l, const float* r, float* fc) {
+int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_void = false) {
   const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
   const Geo g = geo(bc.n, bc.nz);
   Prof prof(p, l == 0 ? 3 : 4);
-  k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n);
+  const float* sd = skip_void ? bc.S + (size_t)(13 * DPN * DPN) * bc.nodes : nullptr;
+  k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
+                                                      (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -228,11 +271,12 @@ int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
   Prof prof(p, l == 0 ? 2 : 4);
   if (l == 0)
     k_prolong_add<DPN, true><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
-                                                                 p->s, p->zm(0), nullptr);
+                                                                 p->s, p->zm(0), nullptr, (ptrdiff_t)bf.nodes,
+                                                                 (ptrdiff_t)bc.nodes);
   else
     k_prolong_add<DPN, false><<<g.grid, g.block, 0, p->stream>>>(
         e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0),
-        bf.S + (size_t)(13 * DPN * DPN) * bf.nodes);
+        bf.S + (size_t)(13 * DPN * DPN) * bf.nodes, (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -244,7 +288,7 @@ int smooth(gmt_problem p, int l, int sweeps) {
   for (int it = 0; it < sweeps; ++it) {
     const float* src = (it & 1) ? b.t : b.u;
     float* dst = (it & 1) ? b.u : b.t;
-    TRY(launch_op<DPN>(p, l, M_JACOBI, src, f, dst, nullptr));
+    TRY(launch_op<DPN>(p, l, M_JACOBI, src, f, dst, nullptr, 1));
   }
   if (sweeps & 1)
     CK(cudaMemcpyAsync(b.u, b.t, b.nodes * p->V * sizeof(float), cudaMemcpyDeviceToDevice, p->stream));
@@ -271,8 +315,8 @@ int vcycle_once(gmt_problem p) {
     LevelBuf& b = p->lv[l];
     LevelBuf& c = p->lv[l + 1];
     TRY(smooth<DPN>(p, l, p->cfg.pre_sweeps));                                  // pre-smoothing
-    TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? nullptr : b.f, b.r, nullptr));  // r = f - K u
-    TRY(launch_restrict<DPN>(p, l, b.r, c.f));                                   // f^{l+1} = R r^l
+    TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? nullptr : b.f, b.r, nullptr, 1));  // r = f - K u
+    TRY(launch_restrict<DPN>(p, l, b.r, c.f, true));                             // f^{l+1} = R r^l
     const size_t vb = c.nodes * p->V * sizeof(float);
     if (c.inj_pending) CK(cudaMemcpyAsync(c.u, c.inj, vb, cudaMemcpyDeviceToDevice, p->stream));
     else CK(cudaMemsetAsync(c.u, 0, vb, p->stream));                             // u^{l+1} = 0 / e_hat
@@ -294,23 +338,44 @@ int build_operators(gmt_problem p) {
   constexpr int ND = Tr<DPN>::ND;
   cudaStream_t st = p->stream;
   const int L = p->L;
+  {
+    Prof prof(p, 6);
+    k_tile_flags<<<dim3(p->tntx, p->tnty, p->lv[0].nz), 128, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz,
+                                                                     p->tntx, p->tnty, p->tflag);
+    LAUNCHED(p);
+  }
+  {
+    // static interface-node list (sorted, deterministic)
+    const size_t total = p->lv[0].nodes;
+    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag);
+    LAUNCHED(p);
+    cub::CountingInputIterator<int> it(0);
+    CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
+    int cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (cnt != p->icount) drop_graph(p);   // grid size of the captured interface launch changes
+    p->icount = cnt;
+  }
   if (L >= 2) {
     LevelBuf& b = p->lv[1];
     const Geo g = geo(b.n, b.nz);
     Prof prof(p, 6);
-    k_stencil_l1<DPN><<<g.grid, g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, p->m1);
+    k_stencil_l1<DPN><<<g.grid, g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz,
+                                                  (float)p->ed.lam, (float)p->ed.mu);
     LAUNCHED(p);
   }
   for (int l = 2; l < L; ++l) {
     LevelBuf& b = p->lv[l];
     const unsigned nelem = (unsigned)b.nodes;
     Prof prof(p, 6);
-    if (l == 2)
-      k_galerkin_elem<DPN, true><<<nelem, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M1g, b.Ke,
-                                                           b.n, b.nz, p->wc);
-    else
-      k_galerkin_elem<DPN, false><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, p->zm(l - 1), p->lv[l - 1].n,
-                                                            p->M1g, b.Ke, b.n, b.nz, p->wc);
+    if (l == 2) {
+      constexpr int TE = 16;
+      k_elem_l2<DPN, TE><<<(nelem + TE - 1) / TE, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g,
+                                                                   b.Ke, b.n, b.nz);
+    } else {
+      k_galerkin_elem<DPN><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc);
+    }
     LAUNCHED(p);
     const Geo g = geo(b.n, b.nz);
     k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz);
@@ -340,9 +405,17 @@ int upload_material(gmt_problem p, const void* material, int dtype, int location
   return GMT_OK;
 }
 
+// Internal vectors keep zeros at inactive nodes so that void warps can skip
+// both reads and writes (k_fine / k_coarse skip_void, k_restrict): r and f
+// are only ever written by kernels that write zeros there, so clearing them
+// whenever the active set may change (new material) restores the invariant.
 int reset_solution(gmt_problem p) {
   for (auto& b : p->lv) {
-    CK(cudaMemsetAsync(b.u, 0, b.nodes * p->V * sizeof(float), p->stream));
+    const size_t vb = b.nodes * p->V * sizeof(float);
+    CK(cudaMemsetAsync(b.u, 0, vb, p->stream));
+    CK(cudaMemsetAsync(b.t, 0, vb, p->stream));
+    if (b.r) CK(cudaMemsetAsync(b.r, 0, vb, p->stream));
+    if (b.f) CK(cudaMemsetAsync(b.f, 0, vb, p->stream));
     b.inj_pending = false;
   }
   return GMT_OK;
@@ -354,9 +427,17 @@ int rebuild(gmt_problem p) {
   return GMT_OK;
 }
 
-int reduce(gmt_problem p, int nblk, int nv) {
-  k_reduce_partials<<<1, 256, 0, p->stream>>>(p->part, nblk, nv, p->red);
+int reduce_launch(gmt_problem p, int nblk, int nv) {
+  double* stage = p->part + p->part_cap - (size_t)RED_BLOCKS * 64;
+  k_reduce_stage<<<RED_BLOCKS, 256, 0, p->stream>>>(p->part, nblk, nv, stage);
   LAUNCHED(p);
+  k_reduce_stage<<<1, 256, 0, p->stream>>>(stage, RED_BLOCKS, nv, p->red);
+  LAUNCHED(p);
+  return GMT_OK;
+}
+
+int reduce(gmt_problem p, int nblk, int nv) {
+  TRY(reduce_launch(p, nblk, nv));
   CK(cudaMemcpyAsync(p->hred, p->red, nv * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   return GMT_OK;
@@ -369,7 +450,8 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
   const Geo g = geo(b.n, b.nz);
   {
     Prof prof(p, 7);
-    k_effective_tensor<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, p->chc, p->part);
+    k_effective_tensor<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
+                                                               (float)p->ed.mu, p->part, (ptrdiff_t)b.nodes);
     LAUNCHED(p);
   }
   TRY(reduce(p, g.nblk, NQ));
@@ -389,8 +471,10 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   constexpr int NR = Tr<DPN>::NR;
   LevelBuf& b = p->lv[0];
   const Geo g = geo(b.n, b.nz);
-  TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part));
-  TRY(reduce(p, g.nblk, 2 * NR));
+  // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
+  // of the tiled kernel followed by those of the interface kernel
+  TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
+  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) + (p->icount + 127) / 128, 2 * NR));
   for (int m = 0; m < NR; ++m) {
     const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[NR + m]);
     if (rel) rel[m] = nf > 0 ? nr_ / nf : nr_;
@@ -405,11 +489,12 @@ int zero_mean(gmt_problem p, float* dst) {
   constexpr int V = Tr<DPN>::V;
   const LevelBuf& b = p->lv[0];
   const Geo g = geo(b.n, b.nz);
-  k_active_sum<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->part);
+  k_active_sum<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->part,
+                                                        (ptrdiff_t)b.nodes);
   LAUNCHED(p);
-  k_reduce_partials<<<1, 256, 0, p->stream>>>(p->part, g.nblk, V + 1, p->red);
-  LAUNCHED(p);
-  k_sub_mean<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->red);
+  TRY(reduce_launch(p, g.nblk, V + 1));
+  k_sub_mean<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->red,
+                                                      (ptrdiff_t)b.nodes);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -431,7 +516,8 @@ void free_all(gmt_problem p) {
     cudaFree(b.u); cudaFree(b.t); cudaFree(b.f); cudaFree(b.r);
     cudaFree(b.S); cudaFree(b.Ke); cudaFree(b.inj);
   }
-  cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->M2g); cudaFree(p->tflag);
+  cudaFree(p->iflag); cudaFree(p->ilist); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
 }
@@ -508,11 +594,12 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   p->nr = p->ed.nrhs;
   p->V = p->dpn * p->nr;
   const int nd = p->ed.nd;
-  for (int i = 0; i < nd * nd; ++i) { p->fc.K[i] = (float)p->ed.K[i]; p->chc.K[i] = (float)p->ed.K[i]; }
-  for (int i = 0; i < nd * p->nr; ++i) { p->fc.F[i] = (float)p->ed.F[i]; p->chc.X0[i] = (float)p->ed.X0[i]; }
+  p->fc.lam = (float)p->ed.lam;
+  p->fc.mu = (float)p->ed.mu;
   p->fc.omega = (float)cfg.omega;
+  std::vector<float> m1(8 * nd * nd);
   for (int j = 0; j < 8; ++j)
-    for (int i = 0; i < nd * nd; ++i) p->m1.M[j * nd * nd + i] = (float)p->ed.M1[j][i];
+    for (int i = 0; i < nd * nd; ++i) m1[j * nd * nd + i] = (float)p->ed.M1[j][i];
   for (int j = 0; j < 8; ++j)
     for (int a = 0; a < 8; ++a)
       for (int A = 0; A < 8; ++A) p->wc.W[(j * 8 + a) * 8 + A] = (float)p->ed.W[j][a][A];
@@ -547,15 +634,46 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if (l >= 2 && (rc = dalloc(p, (void**)&b.Ke, b.nodes * nd * nd * sizeof(float)))) return bail(rc);
     max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
   }
-  p->part_cap = max_blk * 32;
+  p->part_cap = (max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
   if ((rc = dalloc(p, (void**)&p->part, p->part_cap * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->red, 64 * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->s, (size_t)p->N * p->N * p->N * sizeof(float)))) return bail(rc);
+  p->tntx = (cfg.res + TT_X - 1) / TT_X;
+  p->tnty = (cfg.res + TT_Y - 1) / TT_Y;
+  if ((rc = dalloc(p, (void**)&p->tflag, (size_t)p->tntx * p->tnty * p->lv[0].nz))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->iflag, p->lv[0].nodes))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->ilist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->icount_d, sizeof(int)))) return bail(rc);
+  {
+    cub::CountingInputIterator<int> it(0);
+    size_t bytes = 0;
+    if (cub::DeviceSelect::Flagged(nullptr, bytes, it, p->iflag, p->ilist, p->icount_d, (int)p->lv[0].nodes) !=
+        cudaSuccess)
+      return bail(fail(GMT_ERR_CUDA, "cub temp query failed"));
+    p->cub_bytes = bytes;
+    if ((rc = dalloc(p, &p->cub_tmp, bytes))) return bail(rc);
+  }
+  {
+    const int shm3 = TT_NB * Tr<3>::V * TT_PLS * (int)sizeof(float);
+    const int shm1 = TT_NB * Tr<1>::V * TT_PLS * (int)sizeof(float);
+    if (cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))
+      return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
+  }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->M2g, 64 * nd * nd * sizeof(float)))) return bail(rc);
+  {
+    std::vector<float> m2(64 * nd * nd);
+    for (int g = 0; g < 64; ++g)
+      for (int i = 0; i < nd * nd; ++i) m2[g * nd * nd + i] = (float)p->ed.M2[g][i];
+    if (cudaMemcpy(p->M2g, m2.data(), m2.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(GMT_ERR_CUDA, "M2 upload failed"));
+  }
   if (cudaMallocHost(&p->hred, 64 * sizeof(double)) != cudaSuccess)
     return bail(fail(GMT_ERR_NOMEM, "cudaMallocHost failed"));
-  if (cudaMemcpyAsync(p->M1g, p->m1.M, 8 * nd * nd * sizeof(float), cudaMemcpyHostToDevice, p->stream) !=
-      cudaSuccess)
+  if (cudaMemcpy(p->M1g, m1.data(), 8 * nd * nd * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
     return bail(fail(GMT_ERR_CUDA, "M1 upload failed"));
   if ((rc = upload_material(p, material, material_dtype, material_location))) return bail(rc);
   if ((rc = rebuild(p))) return bail(rc);
@@ -714,7 +832,7 @@ int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) 
   TRY(set_device(p));
   LevelBuf& b = p->lv[0];
   const size_t vb = b.nodes * p->V * sizeof(float);
-  float* dst = (location == GMT_DEVICE) ? u : b.r;   // r is scratch between cycles
+  float* dst = (location == GMT_DEVICE) ? u : b.t;   // t is scratch between cycles
   CK(cudaMemcpyAsync(dst, b.u, vb, cudaMemcpyDeviceToDevice, p->stream));
   if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
   if (location == GMT_HOST) {

@@ -30,19 +30,9 @@ __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >
 
 // Kernel parameter blocks: element constants live in the param constant bank,
 // so fully unrolled loops issue FFMA with c[0x0][imm] operands.
-struct FineConsts {      // level 0 (material-driven) operator
-  float K[24 * 24];      // unit-material element matrix
-  float F[24 * 6];       // element loads f_e (App. F1/F2)
-  float omega;
-};
-
-struct M1Consts {        // Galerkin child contributions P_j^T K P_j, 8 children
-  float M[8 * 24 * 24];
-};
-
-struct CHConsts {        // effective-tensor evaluation
-  float K[24 * 24];
-  float X0[24 * 6];
+struct FineConsts {      // level 0 (material-driven) operator: material scalars
+  float lam, mu;         // Lame constants (elastic) / kappa in lam (heat)
+  float omega;           // damped-Jacobi factor
 };
 
 // Block-wide reduction of NV doubles per thread; thread 0 of the block
@@ -74,8 +64,5 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* __re
   }
 }
 
-// Sum `nblk` rows of NV partials in a fixed order: out[k] = sum_b part[b*NV+k].
-__global__ void k_reduce_partials(const double* __restrict__ part, int nblk, int nv,
-                                  double* __restrict__ out);
 
 }  // namespace gmt

@@ -30,12 +30,24 @@ double grad_product(int a, int b, int p, int q) {
 }  // namespace
 
 bool build_element_data(int physics, double E, double nu, double kappa, ElementData* o) {
-  std::memset(o, 0, sizeof(*o));
   if (physics == 0) {
     if (!(E > 0.0) || !(nu > -1.0 && nu < 0.5)) return false;
+    const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double mu = E / (2.0 * (1.0 + nu));
+    return build_element_data_lm(0, lam, mu, 0.0, o);
+  }
+  if (physics == 1) {
+    if (!(kappa > 0.0)) return false;
+    return build_element_data_lm(1, 0.0, 0.0, kappa, o);
+  }
+  return false;
+}
+
+bool build_element_data_lm(int physics, double lam, double mu, double kappa, ElementData* o) {
+  std::memset(o, 0, sizeof(*o));
+  if (physics == 0) {
     o->dpn = 3; o->nrhs = 6;
   } else if (physics == 1) {
-    if (!(kappa > 0.0)) return false;
     o->dpn = 1; o->nrhs = 3;
   } else {
     return false;
@@ -45,8 +57,8 @@ bool build_element_data(int physics, double E, double nu, double kappa, ElementD
   if (physics == 0) {
     // isotropic bilinear form: lam div u div v + 2 mu eps(u):eps(v)
     //   K[(a,p),(b,q)] = lam G_pq + mu (delta_pq tr G + G_qp)
-    const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
-    const double mu = E / (2.0 * (1.0 + nu));
+    o->lam = lam;
+    o->mu = mu;
     for (int a = 0; a < 8; ++a)
       for (int b = 0; b < 8; ++b) {
         double G[3][3];
@@ -66,6 +78,8 @@ bool build_element_data(int physics, double E, double nu, double kappa, ElementD
         for (int c = 0; c < 3; ++c) o->X0[(3 * k + c) * nr + m] = f[m][c];
     }
   } else {
+    o->lam = kappa;
+    o->mu = 0.0;
     for (int a = 0; a < 8; ++a)
       for (int b = 0; b < 8; ++b)
         o->K[a * nd + b] = kappa * (grad_product(a, b, 0, 0) + grad_product(a, b, 1, 1) +
@@ -111,6 +125,67 @@ bool build_element_data(int physics, double E, double nu, double kappa, ElementD
             }
             o->M1[j][(A * dpn + p) * nd + B * dpn + q] = acc;
           }
+  // M2_g = P_j^T M1_i P_j for the 64 fine voxels of a level-2 element
+  for (int g = 0; g < 64; ++g) {
+    const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
+    const int j = (gx >> 1) + 2 * (gy >> 1) + 4 * (gz >> 1);
+    const int i = (gx & 1) + 2 * (gy & 1) + 4 * (gz & 1);
+    for (int A = 0; A < 8; ++A)
+      for (int B = 0; B < 8; ++B)
+        for (int p = 0; p < dpn; ++p)
+          for (int q = 0; q < dpn; ++q) {
+            double acc = 0.0;
+            for (int a = 0; a < 8; ++a) {
+              const double wa = o->W[j][a][A];
+              if (wa == 0.0) continue;
+              for (int b = 0; b < 8; ++b) {
+                const double wb = o->W[j][b][B];
+                if (wb == 0.0) continue;
+                acc += wa * wb * o->M1[i][(a * dpn + p) * nd + b * dpn + q];
+              }
+            }
+            o->M2[g][(A * dpn + p) * nd + B * dpn + q] = acc;
+          }
+  }
+  // Homogeneous block stencil H(d) = sum over the elements e containing node
+  // i and i+d of K[corner_e(i), corner_e(i+d)] (all scales 1).  The kernels
+  // rely on three exact properties, checked here: H(d) is symmetric, H(-d) =
+  // H(d), and entry (p,q), p != q, vanishes unless d is nonzero along both
+  // axes p and q (sign cancellation over the incident elements).
+  double hmax = 0.0;
+  for (int d = 0; d < 27; ++d) {
+    const int dd[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+    for (int p = 0; p < dpn; ++p)
+      for (int q = 0; q < dpn; ++q) {
+        double acc = 0.0;
+        for (int e = 0; e < 8; ++e) {
+          const int ee[3] = {e & 1, (e >> 1) & 1, e >> 2};
+          bool shared = true;
+          for (int a = 0; a < 3; ++a)
+            if ((dd[a] == -1 && ee[a]) || (dd[a] == 1 && !ee[a])) shared = false;
+          if (!shared) continue;
+          const int ki = (1 - ee[0]) + 2 * (1 - ee[1]) + 4 * (1 - ee[2]);
+          const int kj = ki + dd[0] + 2 * dd[1] + 4 * dd[2];
+          acc += o->K[(ki * dpn + p) * nd + kj * dpn + q];
+        }
+        o->H[d * 9 + p * dpn + q] = acc;
+        hmax = std::fmax(hmax, std::fabs(acc));
+      }
+  }
+  const double tol = 1e-13 * (hmax > 0 ? hmax : 1.0);
+  for (int d = 0; d < 27; ++d) {
+    const int dd[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+    for (int p = 0; p < dpn; ++p)
+      for (int q = 0; q < dpn; ++q) {
+        const double h = o->H[d * 9 + p * dpn + q];
+        if (std::fabs(h - o->H[d * 9 + q * dpn + p]) > tol) return false;
+        if (std::fabs(h - o->H[(26 - d) * 9 + p * dpn + q]) > tol) return false;
+        if (p != q && !(dd[p] != 0 && dd[q] != 0)) {
+          if (std::fabs(h) > tol) return false;
+          o->H[d * 9 + p * dpn + q] = 0.0;
+        }
+      }
+  }
   return true;
 }
 

@@ -18,9 +18,16 @@ struct ElementData {
   double F[24 * 6];    // element loads f_e = K X0, nd x nrhs
   double M1[8][24 * 24];  // Galerkin child contributions P_j^T K P_j (Sec. 4.6 Eq. 17)
   double W[8][8][8];      // W[j][a][A]: weight of coarse corner A at child j's corner a
+  double H[27 * 9];       // homogeneous 27-point block stencil: H[d][p][q], all 8 voxels at scale 1
+  double M2[64][24 * 24]; // level-2 Galerkin basis: voxel g = (gx,gy,gz) in [0,4)^3 of a level-2
+                          // element, M2_g = P_j^T M1_i P_j, j = g >> 1, i = g & 1 per axis
+  double lam, mu;         // Lame constants (elastic) / kappa in lam (thermal)
 };
 
 // physics: 0 elastic (E, nu), 1 thermal (kappa).  Returns false on bad input.
 bool build_element_data(int physics, double E, double nu, double kappa, ElementData* out);
+// Same from Lame constants (elastic) / kappa (thermal) without range checks;
+// used for the material-independent unit tables (lam, mu) = (1,0), (0,1).
+bool build_element_data_lm(int physics, double lam, double mu, double kappa, ElementData* out);
 
 }  // namespace gmt

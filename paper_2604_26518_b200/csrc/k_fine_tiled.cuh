@@ -1,0 +1,224 @@
+// Level-0 operator kernel for the V-cycle: z-marching shared-memory tiles.
+//
+// A CTA owns a TT_X x TT_Y column of nodes and marches through a chunk of z
+// planes.  Component planes of u (one-node halo in x and y, periodic wrap)
+// are staged into a ring of TT_NB shared-memory slots with cp.async (16-byte
+// copies for the 32-wide interior rows) while the previous plane is
+// computed, so every u value is read from L2/HBM once per CTA instead of once
+// per neighbour.  Same arithmetic as k_fine (k_op.cuh: void / uniform /
+// interface warp paths, difference form); per-tile activity flags
+// (k_tile_flags) let CTAs skip loading and computing void planes.
+#pragma once
+
+#include "gmt_common.cuh"
+#include "k_level.cuh"
+#include "k_op.cuh"
+
+namespace gmt {
+
+constexpr int TT_X = 32, TT_Y = 4, TT_NB = 4, TT_ZC = 16;
+constexpr int TT_PY = TT_Y + 2;
+constexpr int TT_RS = 40;                 // smem row stride: halo-left at 3, interior at 4..35, halo-right at 36
+constexpr int TT_PLS = TT_PY * TT_RS;     // floats per component plane tile
+
+// flag[(z * nty + ty) * ntx + tx] = 1 if any voxel of voxel-plane z in the
+// tile footprint x in [x0-1, x0+TX-1], y in [y0-1, y0+TY-1] is nonzero.
+__global__ void k_tile_flags(const float* __restrict__ s, ZMap zs, int n, int nz, int ntx, int nty,
+                             uint8_t* __restrict__ flag) {
+  const int tx = blockIdx.x, ty = blockIdx.y, z = blockIdx.z;
+  const int x0 = tx * TT_X, y0 = ty * TT_Y;
+  bool any = false;
+  for (int i = threadIdx.x; i < (TT_X + 1) * (TT_Y + 1); i += blockDim.x) {
+    const int xx = wrapi(x0 - 1 + i % (TT_X + 1), n), yy = wrapi(y0 - 1 + i / (TT_X + 1), n);
+    any |= __ldg(s + ((ptrdiff_t)zs(z) * n + yy) * n + xx) != 0.f;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) flag[((ptrdiff_t)z * nty + ty) * ntx + tx] = any ? 1 : 0;
+}
+
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int DPN, int MODE>
+__global__ void __launch_bounds__(TT_X * TT_Y)
+k_fine_tiled(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu,
+             float* __restrict__ out, int n, int nz, const FineConsts P, double* __restrict__ part,
+             ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
+  static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = T::V;
+  constexpr int NTH = TT_X * TT_Y;
+  extern __shared__ __align__(16) float smem[];   // [TT_NB][V][TT_PY][TT_RS]
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TT_X + tx;
+  const int x0 = blockIdx.x * TT_X, y0 = blockIdx.y * TT_Y;
+  const int z0 = blockIdx.z * TT_ZC, z1 = min(nz, z0 + TT_ZC);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = (x < n) && (y < n);
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  const int xm = wrapi(xc - 1, n), ym = wrapi(yc - 1, n);
+  const bool vec_rows = (x0 + TT_X <= n) && ((n & 3) == 0) && ((cs & 3) == 0);
+
+  auto vflag = [&](int zv) -> bool {   // voxel-plane zv footprint non-void
+    return flag[((ptrdiff_t)zs(zv) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
+  };
+  auto needed = [&](int p) -> bool {   // node plane p read by some active node of planes p-1..p+1
+    return vflag(p - 2) || vflag(p - 1) || vflag(p) || vflag(p + 1);
+  };
+  auto issue = [&](int p) {            // stage node plane p into slot p % NB
+    float* dst = smem + (size_t)((p + 2 * TT_NB) % TT_NB) * V * TT_PLS;
+    const float* src = u + (ptrdiff_t)zu(p) * plane;
+    if (vec_rows) {
+      // per (component, row): 8 x 16-byte interior chunks + 2 halo floats
+      for (int q = tid; q < V * TT_PY * 10; q += NTH) {
+        const int k = q / (TT_PY * 10), rem = q - k * (TT_PY * 10);
+        const int py = rem / 10, c = rem - py * 10;
+        const int gy = wrapi(y0 - 1 + py, n);
+        const float* row = src + k * cs + (ptrdiff_t)gy * n;
+        float* drow = dst + k * TT_PLS + py * TT_RS;
+        if (c < 8) cp_async16(drow + 4 + 4 * c, row + x0 + 4 * c);
+        else if (c == 8) cp_async4(drow + 3, row + wrapi(x0 - 1, n));
+        else cp_async4(drow + 4 + TT_X, row + wrapi(x0 + TT_X, n));
+      }
+    } else {
+      for (int q = tid; q < V * TT_PY * (TT_X + 2); q += NTH) {
+        const int k = q / (TT_PY * (TT_X + 2)), rem = q - k * (TT_PY * (TT_X + 2));
+        const int py = rem / (TT_X + 2), px = rem - py * (TT_X + 2);
+        const int gy = wrapi(y0 - 1 + py, n), gx = wrapi(x0 - 1 + px, n);
+        cp_async4(dst + k * TT_PLS + py * TT_RS + 3 + px, src + k * cs + (ptrdiff_t)gy * n + gx);
+      }
+    }
+  };
+
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+
+  // prologue: planes z0-1, z0, z0+1
+  for (int p = z0 - 1; p <= z0 + 1; ++p) {
+    if (needed(p)) issue(p);
+    cp_async_commit();
+  }
+  for (int z = z0; z < z1; ++z) {
+    if (z + 2 <= z1 && needed(z + 2)) issue(z + 2);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (vflag(z - 1) || vflag(z)) {
+      const float* sl[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) sl[d] = smem + (size_t)((z - 1 + d + 2 * TT_NB) % TT_NB) * V * TT_PLS;
+      const int zs0 = zs(z - 1);
+      auto load_sc = [&](int qx, int qy, float(&sc)[8]) {
+        const int qxm = wrapi(qx - 1, n), qym = wrapi(qy - 1, n);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
+          sc[e] = __ldg(s + (ez ? z : zs0) * plane + (ptrdiff_t)(ey ? qy : qym) * n + (ex ? qx : qxm));
+        }
+      };
+      float sc[8];
+      if (valid) load_sc(xc, yc, sc);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sc[e] = 0.f;
+      }
+      bool act = false, uni = true;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        act |= (sc[e] != 0.f);
+        uni &= (sc[e] == sc[0]);
+      }
+      // homogeneous nodes only; interface nodes (act && !uni) belong to the
+      // static interface list processed by k_iface
+      if (act && uni) {
+        const int base = (ty + 1) * TT_RS + 4 + tx;
+        auto get = [&](int dx, int dy, int dz, int k) -> float {
+          return sl[dz + 1][k * TT_PLS + base + dy * TT_RS + dx];
+        };
+        float acc[V], fl[V], ui[V], D[DPN];
+#pragma unroll
+        for (int k = 0; k < V; ++k) { fl[k] = 0.f; ui[k] = get(0, 0, 0, k); }
+        node_uniform<DPN>(get, sc[0], P.lam, P.mu, ui, acc, D);
+        op_epilogue<DPN, MODE>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, acc, fl, ui, D,
+                               P.omega, nrm, part != nullptr);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
+// Interface nodes: those whose 8 incident voxels are not all equal (the
+// material interface).  flag = 1 per interface node (level 0).
+__global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int nz, uint8_t* __restrict__ flag) {
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  const ptrdiff_t total = plane * nz;
+  for (ptrdiff_t i = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; i < total; i += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % n), y = (int)((i / n) % n), z = (int)(i / plane);
+    const int xm = wrapi(x - 1, n), ym = wrapi(y - 1, n), zm = zs(z - 1);
+    const float s0 = __ldg(s + (ptrdiff_t)zm * plane + (ptrdiff_t)ym * n + xm);
+    bool uni = true;
+#pragma unroll
+    for (int e = 1; e < 8; ++e) {
+      const ptrdiff_t idx = ((e >> 2) ? z : zm) * plane + (ptrdiff_t)(((e >> 1) & 1) ? y : ym) * n + ((e & 1) ? x : xm);
+      uni &= (__ldg(s + idx) == s0);
+    }
+    flag[i] = uni ? 0 : 1;
+  }
+}
+
+// The general (interface) path over the static interface-node list.
+template <int DPN, int MODE>
+__global__ void __launch_bounds__(128)
+k_iface(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu, float* __restrict__ out,
+        int n, int nz, const FineConsts P, double* __restrict__ part, ptrdiff_t cs,
+        const int* __restrict__ list, int count) {
+  static_assert(MODE == M_JACOBI || MODE == M_RESID, "interface kernel: V-cycle modes only");
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = T::V;
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    const ptrdiff_t plane = (ptrdiff_t)n * n;
+    const ptrdiff_t node = list[i];
+    const int x = (int)(node % n), y = (int)((node / n) % n), z = (int)(node / plane);
+    const int xm = wrapi(x - 1, n), xp = wrapi(x + 1, n), ym = wrapi(y - 1, n), yp = wrapi(y + 1, n);
+    const int zm = zu(z - 1), zp = zu(z + 1), zsm = zs(z - 1);
+    float sc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      sc[e] = __ldg(s + ((e >> 2) ? z : zsm) * plane + (ptrdiff_t)(((e >> 1) & 1) ? y : ym) * n + ((e & 1) ? x : xm));
+    auto get = [&](int dx, int dy, int dz, int k) -> float {
+      const int zz = dz < 0 ? zm : (dz > 0 ? zp : z);
+      const int yy = dy < 0 ? ym : (dy > 0 ? yp : y);
+      const int xx = dx < 0 ? xm : (dx > 0 ? xp : x);
+      return __ldg(u + k * cs + ((ptrdiff_t)zz * plane + (ptrdiff_t)yy * n + xx));
+    };
+    float acc[V], fl[V], ui[V], D[DPN];
+#pragma unroll
+    for (int k = 0; k < V; ++k) ui[k] = __ldg(u + k * cs + node);
+    node_general<DPN, true, true>(get, sc, P.lam, P.mu, ui, acc, fl, D);
+    op_epilogue<DPN, MODE>(true, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr);
+  }
+  if (part) block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)blockIdx.x * 2 * NR);
+}
+
+}  // namespace gmt

@@ -3,53 +3,39 @@
 // prolongation + correction, and the single-CTA coarsest-level smoother.
 //
 // Thread mapping: one thread per node, 128-thread blocks tiling (x, y),
-// one z plane per blockIdx.z.  Nodal vectors are [z][y][x][m][c] float32
-// (V = NR*DPN floats per node, 72 B for elasticity), so the 27 neighbour
-// records a thread reads are contiguous 72 B runs shared through L1 with the
-// warp's other nodes.
+// one z plane per blockIdx.z.  Nodal vectors are component planes
+// ("SoA"): value (m, c) of node i lives at base[(m*DPN + c) * cs + i], cs the
+// component stride (n^3, plus ghost planes when slab-partitioned), so every
+// warp-wide access of one component is one coalesced 128-byte line.
 #pragma once
 
 #include "gmt_common.cuh"
+#include "k_op.cuh"
 
 namespace gmt {
 
 enum Mode { M_APPLY = 0, M_RESID = 1, M_JACOBI = 2, M_LOADS = 3, M_DIAG = 4 };
 
 template <int DPN>
-__device__ __forceinline__ void load_node(const float* __restrict__ p, float (&v)[Tr<DPN>::V]) {
-  if constexpr (DPN == 3) {
-    const float2* q = reinterpret_cast<const float2*>(p);
+__device__ __forceinline__ void load_node(const float* __restrict__ p, ptrdiff_t cs,
+                                          float (&v)[Tr<DPN>::V]) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      const float2 t = __ldg(q + k);
-      v[2 * k] = t.x;
-      v[2 * k + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < Tr<DPN>::V; ++k) v[k] = __ldg(p + k);
-  }
+  for (int k = 0; k < Tr<DPN>::V; ++k) v[k] = __ldg(p + k * cs);
 }
 
 template <int DPN>
-__device__ __forceinline__ void store_node(float* __restrict__ p, const float (&v)[Tr<DPN>::V]) {
-  if constexpr (DPN == 3) {
-    float2* q = reinterpret_cast<float2*>(p);
+__device__ __forceinline__ void store_node(float* __restrict__ p, ptrdiff_t cs, const float (&v)[Tr<DPN>::V]) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) q[k] = make_float2(v[2 * k], v[2 * k + 1]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < Tr<DPN>::V; ++k) p[k] = v[k];
-  }
+  for (int k = 0; k < Tr<DPN>::V; ++k) p[k * cs] = v[k];
 }
 
 // Common epilogue of the operator kernels.  acc = (K u)_i, fl = f_i, D = diag.
 template <int DPN, int MODE>
-__device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp,
+__device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp, ptrdiff_t cs,
                                             const float (&acc)[Tr<DPN>::V],
                                             const float (&fl)[Tr<DPN>::V],
                                             const float (&ui)[Tr<DPN>::V], const float (&D)[DPN],
-                                            float omega, double (&nrm)[2 * Tr<DPN>::NR]) {
+                                            float omega, double (&nrm)[2 * Tr<DPN>::NR], bool want_nrm) {
   constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
   float o[V];
 #pragma unroll
@@ -62,28 +48,30 @@ __device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp
       else if (MODE == M_RESID) o[k] = r;
       else if (MODE == M_LOADS) o[k] = fl[k];
       else /* M_JACOBI */ o[k] = D[p] > 0.f ? fmaf(omega / D[p], r, ui[k]) : ui[k];
-      if (MODE == M_RESID || MODE == M_JACOBI) {
-        nrm[m] += valid ? (double)r * (double)r : 0.0;
-        nrm[NR + m] += valid ? (double)fl[k] * (double)fl[k] : 0.0;
+      if ((MODE == M_RESID || MODE == M_JACOBI) && want_nrm && valid) {
+        nrm[m] += (double)r * (double)r;
+        nrm[NR + m] += (double)fl[k] * (double)fl[k];
       }
     }
-  if (valid) store_node<DPN>(outp, o);
+  if (valid) store_node<DPN>(outp, cs, o);
 }
 
 // ---------------------------------------------------------------------------
-// Level 0: the EBE operator of Sec. 4.6 Eq. 14 evaluated from the material.
-// For every neighbour offset d in {-1,0,1}^3 the 27-point block
-//   A(d) = sum_{e containing i and i+d} s_e K_e[corner_e(i), corner_e(i+d)]
-// is formed in registers (shared by all NR load cases) and applied to u_{i+d}.
-// Loads f_i = sum_e s_e f_e[corner_e(i)] (Eq. 3) are formed the same way.
+// Level 0: the EBE operator of Sec. 4.6 Eq. 14 evaluated from the material
+// (thread per node, neighbours through L1; used by the row-level entry points
+// and for small grids -- the V-cycle uses the tiled twin k_fine_tiled).
+// Three warp-uniform paths (the paper's sparse active set, Sec. 4.1.1, at
+// warp granularity): void (nothing to do; with skip_void no reads/writes),
+// uniform (all 8 voxels of every node at one scale: c H(d)), interface
+// (general per-node stencil); see k_op.cuh.
 // ---------------------------------------------------------------------------
 template <int DPN, int MODE>
 __global__ void __launch_bounds__(128)
 k_fine(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu,
        const float* __restrict__ fext, float* __restrict__ out, int n, int nz,
-       const FineConsts P, double* __restrict__ part) {
+       const FineConsts P, double* __restrict__ part, int skip_void, ptrdiff_t cs) {
   using T = Tr<DPN>;
-  constexpr int NR = T::NR, V = T::V, ND = T::ND;
+  constexpr int NR = T::NR, V = T::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   const int z = blockIdx.z;
@@ -91,20 +79,35 @@ k_fine(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap z
   const int xc = valid ? x : 0, yc = valid ? y : 0;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t node = z * plane + (ptrdiff_t)yc * n + xc;
+  const int xm = wrapi(xc - 1, n), xp = wrapi(xc + 1, n);
+  const int ym = wrapi(yc - 1, n), yp = wrapi(yc + 1, n);
+  const int zm = zu(z - 1), zp = zu(z + 1);
 
   float sc[8];
   {
-    const int xs0 = wrapi(xc - 1, n), ys0 = wrapi(yc - 1, n), zs0 = zs(z - 1);
+    const int zs0 = zs(z - 1);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
-      const ptrdiff_t idx = (ez ? z : zs0) * plane + (ptrdiff_t)(ey ? yc : ys0) * n + (ex ? xc : xs0);
+      const ptrdiff_t idx = (ez ? z : zs0) * plane + (ptrdiff_t)(ey ? yc : ym) * n + (ex ? xc : xm);
       sc[e] = valid ? __ldg(s + idx) : 0.f;
     }
   }
-  bool act = false;
+  bool act = false, uni = true;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) act |= (sc[e] != 0.f);
+  for (int e = 0; e < 8; ++e) {
+    act |= (sc[e] != 0.f);
+    uni &= (sc[e] == sc[0]);
+  }
+  const bool warp_act = __any_sync(0xffffffffu, act);
+  const bool warp_uni = __all_sync(0xffffffffu, uni);
+  auto get = [&](int dx, int dy, int dz, int k) -> float {
+    const int zz = dz < 0 ? zm : (dz > 0 ? zp : z);
+    const int yy = dy < 0 ? ym : (dy > 0 ? yp : yc);
+    const int xx = dx < 0 ? xm : (dx > 0 ? xp : xc);
+    return __ldg(u + k * cs + ((ptrdiff_t)zz * plane + (ptrdiff_t)yy * n + xx));
+  };
+  constexpr bool WANT_U = (MODE != M_DIAG && MODE != M_LOADS);
 
   float acc[V], fl[V], ui[V], D[DPN];
 #pragma unroll
@@ -114,84 +117,38 @@ k_fine(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap z
   double nrm[2 * NR];
 #pragma unroll
   for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+  bool do_write = true;
 
-  if (__any_sync(0xffffffffu, act)) {
-    if (MODE != M_LOADS) {
-#pragma unroll
-      for (int dz = -1; dz <= 1; ++dz) {
-        const ptrdiff_t zoff = (ptrdiff_t)zu(z + dz) * plane;
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) {
-          const ptrdiff_t yoff = zoff + (ptrdiff_t)wrapi(yc + dy, n) * n;
-#pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            float A[DPN][DPN];
-#pragma unroll
-            for (int p = 0; p < DPN; ++p)
-#pragma unroll
-              for (int q = 0; q < DPN; ++q) A[p][q] = 0.f;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
-              if ((dx == -1 && ex) || (dx == 1 && !ex) || (dy == -1 && ey) || (dy == 1 && !ey) ||
-                  (dz == -1 && ez) || (dz == 1 && !ez))
-                continue;
-              const int ki = (1 - ex) + 2 * (1 - ey) + 4 * (1 - ez);
-              const int kj = ki + dx + 2 * dy + 4 * dz;
-#pragma unroll
-              for (int p = 0; p < DPN; ++p)
-#pragma unroll
-                for (int q = 0; q < DPN; ++q)
-                  A[p][q] = fmaf(sc[e], P.K[(ki * DPN + p) * ND + kj * DPN + q], A[p][q]);
-            }
-            if (dx == 0 && dy == 0 && dz == 0) {
-#pragma unroll
-              for (int p = 0; p < DPN; ++p) D[p] = A[p][p];
-            }
-            if (MODE != M_DIAG) {
-              float uj[V];
-              load_node<DPN>(u + (yoff + wrapi(xc + dx, n)) * V, uj);
-              if (dx == 0 && dy == 0 && dz == 0) {
-#pragma unroll
-                for (int k = 0; k < V; ++k) ui[k] = uj[k];
-              }
-#pragma unroll
-              for (int m = 0; m < NR; ++m)
-#pragma unroll
-                for (int p = 0; p < DPN; ++p)
-#pragma unroll
-                  for (int q = 0; q < DPN; ++q)
-                    acc[m * DPN + p] = fmaf(A[p][q], uj[m * DPN + q], acc[m * DPN + p]);
-            }
-          }
-        }
-      }
-    }
-    if ((MODE == M_RESID || MODE == M_JACOBI || MODE == M_LOADS) && !fext) {
-      {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int ki = (1 - (e & 1)) + 2 * (1 - ((e >> 1) & 1)) + 4 * (1 - (e >> 2));
-#pragma unroll
-          for (int m = 0; m < NR; ++m)
-#pragma unroll
-            for (int p = 0; p < DPN; ++p)
-              fl[m * DPN + p] = fmaf(sc[e], P.F[(ki * DPN + p) * NR + m], fl[m * DPN + p]);
-        }
-      }
-    }
-  } else if (MODE == M_JACOBI) {
-    if (valid) load_node<DPN>(u + node * V, ui);   // whole warp inactive: copy through
-  }
-  if ((MODE == M_RESID || MODE == M_JACOBI) && fext && valid) load_node<DPN>(fext + node * V, fl);
-
-  if (MODE == M_DIAG) {
-    if (valid) {
-#pragma unroll
-      for (int p = 0; p < DPN; ++p) out[node * DPN + p] = D[p];
-    }
+  if (!warp_act) {
+    if (skip_void) do_write = false;
+    else if (MODE == M_JACOBI && valid) load_node<DPN>(u + node, cs, ui);
   } else {
-    op_epilogue<DPN, MODE>(valid, out + node * V, acc, fl, ui, D, P.omega, nrm);
+    if (WANT_U || MODE == M_JACOBI) load_node<DPN>(u + node, cs, ui);
+    if (warp_uni) {
+      if (WANT_U) node_uniform<DPN>(get, sc[0], P.lam, P.mu, ui, acc, D);
+      else {
+#pragma unroll
+        for (int p = 0; p < DPN; ++p) {
+          const int i = 13 * DPN * DPN + p * DPN + p;
+          D[p] = sc[0] * (CT<DPN>::two ? fmaf(P.lam, CT<DPN>::Hl(i), P.mu * CT<DPN>::Hm(i)) : P.lam * CT<DPN>::Hl(i));
+        }
+      }
+    } else {
+      node_general<DPN, true, WANT_U>(get, sc, P.lam, P.mu, ui, acc, fl, D);
+    }
+  }
+  if ((MODE == M_RESID || MODE == M_JACOBI) && fext && valid && do_write)
+    load_node<DPN>(fext + node, cs, fl);
+
+  if (do_write) {
+    if (MODE == M_DIAG) {
+      if (valid) {
+#pragma unroll
+        for (int p = 0; p < DPN; ++p) out[p * cs + node] = D[p];
+      }
+    } else {
+      op_epilogue<DPN, MODE>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr);
+    }
   }
   if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
     const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -207,7 +164,7 @@ template <int DPN, int MODE>
 __global__ void __launch_bounds__(128)
 k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
          const float* __restrict__ f, float* __restrict__ out, int n, int nz, float omega,
-         double* __restrict__ part) {
+         double* __restrict__ part, int skip_void, ptrdiff_t cs) {
   using T = Tr<DPN>;
   constexpr int NR = T::NR, V = T::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,7 +190,9 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
 #pragma unroll
   for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
 
-  if (__any_sync(0xffffffffu, act)) {
+  const bool warp_act = __any_sync(0xffffffffu, act);
+  const bool do_write = warp_act || !skip_void;
+  if (warp_act) {
     if (MODE != M_DIAG && MODE != M_LOADS) {
 #pragma unroll
       for (int d = 0; d < 27; ++d) {
@@ -246,31 +205,34 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
             A[p][q] = valid ? __ldg(S + ((d * DPN + p) * DPN + q) * nodes + node) : 0.f;
         float uj[V];
         load_node<DPN>(u + ((ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(yc + dy, n) * n +
-                            wrapi(xc + dx, n)) * V, uj);
+                            wrapi(xc + dx, n)), cs, uj);
         if (d == 13) {
 #pragma unroll
           for (int k = 0; k < V; ++k) ui[k] = uj[k];
         }
 #pragma unroll
-        for (int m = 0; m < NR; ++m)
+        for (int p = 0; p < DPN; ++p)
 #pragma unroll
-          for (int p = 0; p < DPN; ++p)
+          for (int q = 0; q < DPN; ++q) {
+            const float a = A[p][q];
 #pragma unroll
-            for (int q = 0; q < DPN; ++q)
-              acc[m * DPN + p] = fmaf(A[p][q], uj[m * DPN + q], acc[m * DPN + p]);
+            for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, uj[m * DPN + q], acc[m * DPN + p]);
+          }
       }
     }
-  } else if (MODE == M_JACOBI) {
-    if (valid) load_node<DPN>(u + node * V, ui);
+  } else if (MODE == M_JACOBI && do_write) {
+    if (valid) load_node<DPN>(u + node, cs, ui);
   }
-  if ((MODE == M_RESID || MODE == M_JACOBI) && valid) load_node<DPN>(f + node * V, fl);
-  if (MODE == M_DIAG) {
-    if (valid) {
+  if ((MODE == M_RESID || MODE == M_JACOBI) && valid && do_write) load_node<DPN>(f + node, cs, fl);
+  if (do_write) {
+    if (MODE == M_DIAG) {
+      if (valid) {
 #pragma unroll
-      for (int p = 0; p < DPN; ++p) out[node * DPN + p] = D[p];
+        for (int p = 0; p < DPN; ++p) out[p * cs + node] = D[p];
+      }
+    } else {
+      op_epilogue<DPN, MODE>(valid, out + node, cs, acc, fl, ui, D, omega, nrm, part != nullptr);
     }
-  } else {
-    op_epilogue<DPN, MODE>(valid, out + node * V, acc, fl, ui, D, omega, nrm);
   }
   if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
     const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -284,12 +246,19 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
 // ---------------------------------------------------------------------------
 template <int DPN>
 __global__ void __launch_bounds__(128)
-k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc, int nzc, int nf) {
+k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc, int nzc, int nf,
+           const float* __restrict__ Sdiag_c, ptrdiff_t csf, ptrdiff_t csc) {
   constexpr int V = Tr<DPN>::V;
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
   const int Z = blockIdx.z;
-  if (X >= nc || Y >= nc) return;
+  const bool valid = X < nc && Y < nc;
+  if (Sdiag_c) {
+    // skip warps of inactive coarse nodes (f_c stays 0 there: R r = 0)
+    const bool act = valid && __ldg(Sdiag_c + ((ptrdiff_t)Z * nc + Y) * nc + X) != 0.f;
+    if (!__any_sync(0xffffffffu, act)) return;
+  }
+  if (!valid) return;
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   float acc[V];
 #pragma unroll
@@ -304,11 +273,11 @@ k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc,
         const ptrdiff_t i = (ptrdiff_t)zf(2 * Z + dz) * pf + (ptrdiff_t)wrapi(2 * Y + dy, nf) * nf +
                             wrapi(2 * X + dx, nf);
         float v[V];
-        load_node<DPN>(r + i * V, v);
+        load_node<DPN>(r + i, csf, v);
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = fmaf(w, v[k], acc[k]);
       }
-  store_node<DPN>(fc + ((ptrdiff_t)Z * nc * nc + (ptrdiff_t)Y * nc + X) * V, acc);
+  store_node<DPN>(fc + ((ptrdiff_t)Z * nc * nc + (ptrdiff_t)Y * nc + X), csc, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -320,7 +289,8 @@ k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc,
 template <int DPN, bool FINE0>
 __global__ void __launch_bounds__(128)
 k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int nf, int nzf, int nc,
-              const float* __restrict__ s, ZMap zs, const float* __restrict__ Sdiag) {
+              const float* __restrict__ s, ZMap zs, const float* __restrict__ Sdiag, ptrdiff_t csf,
+              ptrdiff_t csc) {
   constexpr int V = Tr<DPN>::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -346,7 +316,7 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
   const int X1 = wrapi(X0 + 1, nc), Y1 = wrapi(Y0 + 1, nc), Z1 = zc(Z0 + 1);
   const ptrdiff_t pc = (ptrdiff_t)nc * nc;
   float acc[V];
-  load_node<DPN>(u + node * V, acc);
+  load_node<DPN>(u + node, csf, acc);
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
     const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
@@ -354,11 +324,11 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
     const float w = (rx ? 0.5f : 1.f) * (ry ? 0.5f : 1.f) * (rz ? 0.5f : 1.f);
     const ptrdiff_t ic = (ptrdiff_t)(oz ? Z1 : Z0) * pc + (ptrdiff_t)(oy ? Y1 : Y0) * nc + (ox ? X1 : X0);
     float v[V];
-    load_node<DPN>(e + ic * V, v);
+    load_node<DPN>(e + ic, csc, v);
 #pragma unroll
     for (int k = 0; k < V; ++k) acc[k] = fmaf(w, v[k], acc[k]);
   }
-  store_node<DPN>(u + node * V, acc);
+  store_node<DPN>(u + node, csf, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -394,7 +364,7 @@ k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, f
           for (int p = 0; p < DPN; ++p)
 #pragma unroll
             for (int q = 0; q < DPN; ++q)
-              acc[m * DPN + p] = fmaf(A[p][q], src[j * V + m * DPN + q], acc[m * DPN + p]);
+              acc[m * DPN + p] = fmaf(A[p][q], src[(m * DPN + q) * nodes + j], acc[m * DPN + p]);
       }
 #pragma unroll
       for (int m = 0; m < NR; ++m)
@@ -402,8 +372,8 @@ k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, f
         for (int p = 0; p < DPN; ++p) {
           const int k = m * DPN + p;
           const float Dp = S[((13 * DPN + p) * DPN + p) * nodes + i];
-          const float ui = src[i * V + k];
-          dst[i * V + k] = Dp > 0.f ? fmaf(omega / Dp, f[i * V + k] - acc[k], ui) : ui;
+          const float ui = src[k * nodes + i];
+          dst[k * nodes + i] = Dp > 0.f ? fmaf(omega / Dp, f[k * nodes + i] - acc[k], ui) : ui;
         }
     }
     __syncthreads();

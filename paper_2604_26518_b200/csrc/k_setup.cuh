@@ -12,7 +12,10 @@
 // Element matrices are SoA: Ke[(r*ND + c) * nelem + E] (coalesced over x).
 #pragma once
 
+#include <utility>
+
 #include "gmt_common.cuh"
+#include "gmt_consts.cuh"
 
 namespace gmt {
 
@@ -26,113 +29,170 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ 
 }
 
 // Level-1 stencil from the material.  Thread per level-1 node I = (X,Y,Z);
-// the 8 coarse elements around I cover fine voxels [2X-2, 2X+1]^3.
+// the 8 coarse elements around I cover fine voxels [2X-2, 2X+1]^3.  Each of
+// the 27 offset blocks is its own template instantiation so every M1 index is
+// a compile-time constant.
+template <int DPN, int D>
+__device__ __forceinline__ void l1_block(const float (&sv)[64], float lam, float mu, float* __restrict__ S,
+                                         ptrdiff_t nodes, ptrdiff_t node) {
+  constexpr int ND = Tr<DPN>::ND;
+  constexpr int dx = D % 3 - 1, dy = (D / 3) % 3 - 1, dz = D / 9 - 1;
+  float Al[DPN][DPN], Am[DPN][DPN];
+#pragma unroll
+  for (int p = 0; p < DPN; ++p)
+#pragma unroll
+    for (int q = 0; q < DPN; ++q) Al[p][q] = Am[p][q] = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
+    if ((dx == -1 && ex) || (dx == 1 && !ex) || (dy == -1 && ey) || (dy == 1 && !ey) ||
+        (dz == -1 && ez) || (dz == 1 && !ez))
+      continue;
+    const int kI = (1 - ex) + 2 * (1 - ey) + 4 * (1 - ez);
+    const int kJ = kI + dx + 2 * dy + 4 * dz;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jx = j & 1, jy = (j >> 1) & 1, jz = j >> 2;
+      const float sj = sv[((2 * ez + jz) * 4 + 2 * ey + jy) * 4 + 2 * ex + jx];
+#pragma unroll
+      for (int p = 0; p < DPN; ++p)
+#pragma unroll
+        for (int q = 0; q < DPN; ++q) {
+          const int i = j * ND * ND + (kI * DPN + p) * ND + kJ * DPN + q;
+          Al[p][q] = fmaf(sj, CT<DPN>::M1l(i), Al[p][q]);
+          if (CT<DPN>::two) Am[p][q] = fmaf(sj, CT<DPN>::M1m(i), Am[p][q]);
+        }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < DPN; ++p)
+#pragma unroll
+    for (int q = 0; q < DPN; ++q)
+      S[((D * DPN + p) * DPN + q) * nodes + node] = CT<DPN>::two ? fmaf(lam, Al[p][q], mu * Am[p][q]) : lam * Al[p][q];
+}
+
+template <int DPN, int... Ds>
+__device__ __forceinline__ void l1_all(std::integer_sequence<int, Ds...>, const float (&sv)[64], float lam,
+                                       float mu, float* __restrict__ S, ptrdiff_t nodes, ptrdiff_t node) {
+  (l1_block<DPN, Ds>(sv, lam, mu, S, nodes, node), ...);
+}
+
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc,
-             const M1Consts M) {
-  constexpr int ND = Tr<DPN>::ND;
+             float lam, float mu) {
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
   const int Z = blockIdx.z;
-  if (X >= nc || Y >= nc) return;
+  const bool valid = X < nc && Y < nc;
+  const int Xc = valid ? X : 0, Yc = valid ? Y : 0;
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   float sv[64];
+  bool any = false;
 #pragma unroll
   for (int fz = 0; fz < 4; ++fz) {
     const ptrdiff_t zo = (ptrdiff_t)zs(2 * Z - 2 + fz) * pf;
 #pragma unroll
     for (int fy = 0; fy < 4; ++fy) {
-      const ptrdiff_t yo = zo + (ptrdiff_t)wrapi(2 * Y - 2 + fy, nf) * nf;
+      const ptrdiff_t yo = zo + (ptrdiff_t)wrapi(2 * Yc - 2 + fy, nf) * nf;
 #pragma unroll
-      for (int fx = 0; fx < 4; ++fx) sv[(fz * 4 + fy) * 4 + fx] = __ldg(s + yo + wrapi(2 * X - 2 + fx, nf));
+      for (int fx = 0; fx < 4; ++fx) {
+        const float v = __ldg(s + yo + wrapi(2 * Xc - 2 + fx, nf));
+        sv[(fz * 4 + fy) * 4 + fx] = v;
+        any |= (v != 0.f);
+      }
     }
   }
   const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
-  const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
-#pragma unroll
-  for (int d = 0; d < 27; ++d) {
-    const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
-    float A[DPN][DPN];
-#pragma unroll
-    for (int p = 0; p < DPN; ++p)
-#pragma unroll
-      for (int q = 0; q < DPN; ++q) A[p][q] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
-      if ((dx == -1 && ex) || (dx == 1 && !ex) || (dy == -1 && ey) || (dy == 1 && !ey) ||
-          (dz == -1 && ez) || (dz == 1 && !ez))
-        continue;
-      const int kI = (1 - ex) + 2 * (1 - ey) + 4 * (1 - ez);
-      const int kJ = kI + dx + 2 * dy + 4 * dz;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int jx = j & 1, jy = (j >> 1) & 1, jz = j >> 2;
-        const float sj = sv[((2 * ez + jz) * 4 + 2 * ey + jy) * 4 + 2 * ex + jx];
-#pragma unroll
-        for (int p = 0; p < DPN; ++p)
-#pragma unroll
-          for (int q = 0; q < DPN; ++q)
-            A[p][q] = fmaf(sj, M.M[j * ND * ND + (kI * DPN + p) * ND + kJ * DPN + q], A[p][q]);
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < DPN; ++p)
-#pragma unroll
-      for (int q = 0; q < DPN; ++q) S[((d * DPN + p) * DPN + q) * nodes + node] = A[p][q];
+  const ptrdiff_t node = ((ptrdiff_t)Z * nc + Yc) * nc + Xc;
+  if (!__any_sync(0xffffffffu, any)) {       // void warp: all-zero stencil
+    if (valid)
+      for (int k = 0; k < 27 * DPN * DPN; ++k) S[k * nodes + node] = 0.f;
+    return;
   }
+  if (!valid) return;
+  l1_all<DPN>(std::make_integer_sequence<int, 27>{}, sv, lam, mu, S, nodes, node);
 }
 
-// Galerkin element matrices of level lc >= 2 from the children at level lc-1:
-//   K_E = sum_j P_j^T K_{child j} P_j   (Sec. 4.6 Eq. 17, patch form).
-// One CTA per coarse element, ND*ND threads (thread = output entry (r, c)).
-// FROM_MATERIAL: children are level-1 elements, K_child = sum_i s_i M1_i.
-template <int DPN, bool FROM_MATERIAL>
+// Level-2 Galerkin element matrices straight from the material:
+//   K_E = sum_{g in 4x4x4 fine voxels of E} s_g M2_g,  M2_g = P_j^T M1_i P_j
+// (g = child j's voxel i; Sec. 4.6 Eq. 17 applied twice).  One CTA per tile of
+// TE elements, one thread per matrix entry; each M2 value fetched once per
+// tile and applied to TE elements held in shared memory.
+template <int DPN, int TE>
+__global__ void __launch_bounds__(Tr<DPN>::ND * Tr<DPN>::ND)
+k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict__ M2,
+          float* __restrict__ dst, int n2, int nz2) {
+  constexpr int NT = Tr<DPN>::ND * Tr<DPN>::ND;
+  __shared__ __align__(16) float sg[64][TE];
+  const int t = threadIdx.x;
+  const ptrdiff_t nelem = (ptrdiff_t)n2 * n2 * nz2;
+  const ptrdiff_t E0 = (ptrdiff_t)blockIdx.x * TE;
+  bool any = false;
+  for (int i = t; i < 64 * TE; i += NT) {
+    const int e = i % TE, g = i / TE;
+    const ptrdiff_t E = E0 + e;
+    float v = 0.f;
+    if (E < nelem) {
+      const int X = (int)(E % n2), Y = (int)((E / n2) % n2), Z = (int)(E / ((ptrdiff_t)n2 * n2));
+      const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
+      v = __ldg(s + ((ptrdiff_t)zs(4 * Z + gz) * n0 + 4 * Y + gy) * n0 + 4 * X + gx);
+    }
+    sg[g][e] = v;
+    any |= (v != 0.f);
+  }
+  const bool tile_any = __syncthreads_or(any);
+  float acc[TE];
+#pragma unroll
+  for (int e = 0; e < TE; ++e) acc[e] = 0.f;
+  if (tile_any) {
+#pragma unroll 4
+    for (int g = 0; g < 64; ++g) {
+      const float m = __ldg(M2 + g * NT + t);
+#pragma unroll
+      for (int e = 0; e < TE; e += 4) {
+        const float4 sv = *reinterpret_cast<const float4*>(&sg[g][e]);
+        acc[e] = fmaf(sv.x, m, acc[e]);
+        acc[e + 1] = fmaf(sv.y, m, acc[e + 1]);
+        acc[e + 2] = fmaf(sv.z, m, acc[e + 2]);
+        acc[e + 3] = fmaf(sv.w, m, acc[e + 3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < TE; ++e)
+    if (E0 + e < nelem) dst[(ptrdiff_t)t * nelem + E0 + e] = acc[e];
+}
+
+// Galerkin element matrices of level lc >= 3 from the stored children:
+//   K_E = sum_j P_j^T K_{child j} P_j   (Sec. 4.6 Eq. 17, patch form),
+// two stages per child through shared memory: T = K_child P_j, K_E += P_j^T T.
+// One CTA per coarse element, ND*ND threads (thread = matrix entry).
+template <int DPN>
 __global__ void __launch_bounds__(576)
-k_galerkin_elem(const float* __restrict__ src, ZMap zsrc, int nsrc_res,
-                const float* __restrict__ M1g, float* __restrict__ dst, int nc, int nzc,
-                const WConsts Wt) {
+k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, int nzc, const WConsts Wt) {
   constexpr int ND = Tr<DPN>::ND;
-  __shared__ float Kc[ND * ND];
-  __shared__ float sch[8];
+  __shared__ float Kc[ND * ND], Tm[ND * ND];
   const int t = threadIdx.x;
   const int r = t / ND, c = t % ND;
   const int A = r / DPN, p = r % DPN, B = c / DPN, q = c % DPN;
   const int E = blockIdx.x;
   const int X = E % nc, Y = (E / nc) % nc, Z = E / (nc * nc);
   const ptrdiff_t nelem_c = (ptrdiff_t)nc * nc * nzc;
-  const int nfr = 2 * nc;  // child (level lc-1) resolution
+  const int nfr = 2 * nc;
+  const ptrdiff_t nelem_f = (ptrdiff_t)nfr * nfr * (2 * nzc);
   float acc = 0.f;
   for (int j = 0; j < 8; ++j) {
     const int cx = 2 * X + (j & 1), cy = 2 * Y + ((j >> 1) & 1), cz = 2 * Z + (j >> 2);
-    if (FROM_MATERIAL) {
-      // child (level-1 element) covers fine voxels 2*(cx,cy,cz) + {0,1}^3
-      if (t < 8) {
-        const int fx = 2 * cx + (t & 1), fy = 2 * cy + ((t >> 1) & 1), fz = 2 * cz + (t >> 2);
-        sch[t] = __ldg(src + ((ptrdiff_t)zsrc(fz) * nsrc_res + fy) * nsrc_res + fx);
-      }
-      __syncthreads();
-      float v = 0.f;
+    Kc[t] = __ldg(src + (ptrdiff_t)t * nelem_f + ((ptrdiff_t)cz * nfr + cy) * nfr + cx);
+    __syncthreads();
+    float tv = 0.f;   // T[(a p)][(B q)], here r = (a p)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v = fmaf(sch[i], __ldg(M1g + i * ND * ND + t), v);
-      Kc[t] = v;
-    } else {
-      const ptrdiff_t nelem_f = (ptrdiff_t)nfr * nfr * (2 * nzc);
-      Kc[t] = __ldg(src + (ptrdiff_t)t * nelem_f + ((ptrdiff_t)cz * nfr + cy) * nfr + cx);
-    }
+    for (int b = 0; b < 8; ++b) tv = fmaf(Wt.W[(j * 8 + b) * 8 + B], Kc[r * ND + b * DPN + q], tv);
+    Tm[t] = tv;
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const float wa = Wt.W[(j * 8 + a) * 8 + A];
-      if (wa == 0.f) continue;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const float wb = Wt.W[(j * 8 + b) * 8 + B];
-        if (wb == 0.f) continue;
-        acc = fmaf(wa * wb, Kc[(a * DPN + p) * ND + b * DPN + q], acc);
-      }
-    }
+    for (int a = 0; a < 8; ++a) acc = fmaf(Wt.W[(j * 8 + a) * 8 + A], Tm[(a * DPN + p) * ND + c], acc);
     __syncthreads();
   }
   dst[(ptrdiff_t)t * nelem_c + E] = acc;

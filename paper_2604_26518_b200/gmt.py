@@ -4,8 +4,8 @@ fallback -- loading fails loudly when libgmt.so is missing.
 
 Arrays: numpy arrays are passed as host buffers (GMT_HOST); torch CUDA
 tensors as device buffers (GMT_DEVICE).  Nodal vectors are float32
-[z, y, x, m, c] (m = load case, c = component); material fields float32
-or uint8 [z, y, x].
+component planes [m, c, z, y, x] (m = load case, c = component); material
+fields float32 or uint8 [z, y, x].
 """
 from __future__ import annotations
 
@@ -193,7 +193,7 @@ class Problem:
 
     def vec_shape(self, level: int = 0):
         n = self.level_res(level)
-        return (n, n, n, self.nrhs, self.dpn)
+        return (self.nrhs, self.dpn, n, n, n)
 
     @property
     def stream(self) -> int:

@@ -212,12 +212,12 @@ def batch_truss_psl(n: int, count: int, seed: int = 0):
 def initial_guess(n: int, nrhs: int, dpn: int, seed: int = 0, amp: float = 0.1,
                   material: np.ndarray | None = None) -> np.ndarray:
     """A smooth, seeded synthetic warm start u_hat^1 (Alg. 2 line 1 input),
-    layout [z, y, x, m, c] float32; zero on nodes whose 8 surrounding voxels
-    are all void when ``material`` is given.  Stands in for the network
-    prediction, which is out of scope."""
+    layout [m, c, z, y, x] float32 (component planes); zero on nodes whose 8
+    surrounding voxels are all void when ``material`` is given.  Stands in
+    for the network prediction, which is out of scope."""
     rng = np.random.default_rng(seed)
     t = _axes(n)
-    out = np.zeros((n, n, n, nrhs, dpn), dtype=np.float32)
+    out = np.zeros((nrhs, dpn, n, n, n), dtype=np.float32)
     for m in range(nrhs):
         for c in range(dpn):
             a = rng.standard_normal(3)
@@ -225,7 +225,7 @@ def initial_guess(n: int, nrhs: int, dpn: int, seed: int = 0, amp: float = 0.1,
             fx = np.sin(_TWO_PI * t + ph[0]) * a[0]
             fy = np.sin(_TWO_PI * t + ph[1]) * a[1]
             fz = np.sin(_TWO_PI * t + ph[2]) * a[2]
-            out[..., m, c] = amp * (fz[:, None, None] + fy[None, :, None] + fx[None, None, :])
+            out[m, c] = amp * (fz[:, None, None] + fy[None, :, None] + fx[None, None, :])
     if material is not None:
         occ = material > 0
         act = np.zeros_like(occ)
@@ -233,7 +233,7 @@ def initial_guess(n: int, nrhs: int, dpn: int, seed: int = 0, amp: float = 0.1,
             for dy in (0, 1):
                 for dx in (0, 1):
                     act |= np.roll(occ, shift=(dz, dy, dx), axis=(0, 1, 2))
-        out[~act] = 0.0
+        out[:, :, ~act] = 0.0
     return out
 
 

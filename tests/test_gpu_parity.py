@@ -34,6 +34,18 @@ def _problem(s, kind, levels, **kw):
     return Problem(np.ascontiguousarray(s, dtype=np.float32), physics=kind, levels=levels, **kw)
 
 
+def to_gpu(u, n, dpn):
+    """oracle (ndof, M), dof = node*dpn + c  ->  GPU component planes [m, c, z, y, x]"""
+    M = u.shape[1]
+    return np.ascontiguousarray(u.reshape(n, n, n, dpn, M).transpose(4, 3, 0, 1, 2))
+
+
+def from_gpu(a):
+    """GPU [m, c, z, y, x] -> oracle (ndof, M)"""
+    M, dpn, n = a.shape[0], a.shape[1], a.shape[2]
+    return np.asarray(a, dtype=np.float64).transpose(2, 3, 4, 1, 0).reshape(n ** 3 * dpn, M)
+
+
 def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
@@ -84,8 +96,8 @@ def test_loads(case):
     n = s.shape[0]
     f = torch.empty(P.vec_shape(0), device="cuda")
     P.gmt_op_loads(f)
-    want = fem.to_node_layout(H.f, n, ph.dpn)
-    scale = fem.to_node_layout(fem.assemble_f(s, _abs_phys(ph)), n, ph.dpn)
+    want = to_gpu(H.f, n, ph.dpn)
+    scale = to_gpu(fem.assemble_f(s, _abs_phys(ph)), n, ph.dpn)
     _close(_host(f), want, np.abs(scale) + 1e-7)
 
 
@@ -111,29 +123,29 @@ def test_apply_residual_jacobi(case, level):
     n = H.n[level]
     u = _rand(H, level)
     f = _rand(H, level, seed=99)
-    scale = fem.to_node_layout(_absK(H, level) @ np.abs(u), n, ph.dpn)
-    ud = _dev(fem.to_node_layout(u, n, ph.dpn))
+    scale = to_gpu(_absK(H, level) @ np.abs(u), n, ph.dpn)
+    ud = _dev(to_gpu(u, n, ph.dpn))
     y = torch.empty_like(ud)
     # apply
     P.gmt_op_apply(level, ud, y)
-    _close(_host(y), fem.to_node_layout(H.K[level] @ u, n, ph.dpn), scale)
+    _close(_host(y), to_gpu(H.K[level] @ u, n, ph.dpn), scale)
     # residual (level 0 with the built-in loads; coarse levels with explicit f)
     if level == 0:
         P.gmt_op_residual(0, ud, None, y)
         want = H.f - H.K[0] @ u
-        sc = scale + np.abs(fem.to_node_layout(H.f, n, ph.dpn))
+        sc = scale + np.abs(to_gpu(H.f, n, ph.dpn))
     else:
-        P.gmt_op_residual(level, ud, _dev(fem.to_node_layout(f, n, ph.dpn)), y)
+        P.gmt_op_residual(level, ud, _dev(to_gpu(f, n, ph.dpn)), y)
         want = f - H.K[level] @ u
-        sc = scale + np.abs(fem.to_node_layout(f, n, ph.dpn))
-    _close(_host(y), fem.to_node_layout(want, n, ph.dpn), sc)
+        sc = scale + np.abs(to_gpu(f, n, ph.dpn))
+    _close(_host(y), to_gpu(want, n, ph.dpn), sc)
     # one damped-Jacobi sweep
     fl = H.f if level == 0 else f
-    P.gmt_op_jacobi(level, ud, None if level == 0 else _dev(fem.to_node_layout(f, n, ph.dpn)), y)
+    P.gmt_op_jacobi(level, ud, None if level == 0 else _dev(to_gpu(f, n, ph.dpn)), y)
     want = gmg.jacobi(H.K[level], H.Dinv[level], u, fl, OMEGA[kind], 1)
-    dsc = np.abs(H.Dinv[level])[:, None] * fem.from_node_layout(sc)
-    _close(_host(y), fem.to_node_layout(want, n, ph.dpn),
-           fem.to_node_layout(np.abs(u) + OMEGA[kind] * dsc, n, ph.dpn))
+    dsc = np.abs(H.Dinv[level])[:, None] * from_gpu(sc)
+    _close(_host(y), to_gpu(want, n, ph.dpn),
+           to_gpu(np.abs(u) + OMEGA[kind] * dsc, n, ph.dpn))
 
 
 def test_diagonal_and_galerkin_stencil(case):
@@ -142,9 +154,9 @@ def test_diagonal_and_galerkin_stencil(case):
     dpn = ph.dpn
     for l in range(H.L):
         n = H.n[l]
-        d = torch.empty((n, n, n, dpn), device="cuda")
+        d = torch.empty((dpn, n, n, n), device="cuda")
         P.gmt_op_diagonal(l, d)
-        want = H.K[l].diagonal().reshape(n, n, n, dpn)
+        want = H.K[l].diagonal().reshape(n, n, n, dpn).transpose(3, 0, 1, 2)
         _close(_host(d), want, np.abs(want).max() * np.ones_like(want), rtol=1e-5)
         if l == 0 or n < 3:
             continue
@@ -170,17 +182,17 @@ def test_restrict_and_prolong(case):
         nf, nc = H.n[l], H.n[l + 1]
         r = _rand(H, l, seed=5) * H.active[l][:, None]
         fc = torch.empty(P.vec_shape(l + 1), device="cuda")
-        P.gmt_op_restrict(l, _dev(fem.to_node_layout(r, nf, ph.dpn)), fc)
+        P.gmt_op_restrict(l, _dev(to_gpu(r, nf, ph.dpn)), fc)
         want = H.P[l].T @ r
-        _close(_host(fc), fem.to_node_layout(want, nc, ph.dpn),
-               fem.to_node_layout(abs(H.P[l]).T @ np.abs(r), nc, ph.dpn) + 1e-30)
+        _close(_host(fc), to_gpu(want, nc, ph.dpn),
+               to_gpu(abs(H.P[l]).T @ np.abs(r), nc, ph.dpn) + 1e-30)
         e = _rand(H, l + 1, seed=6)
         u = _rand(H, l, seed=7)
-        ud = _dev(fem.to_node_layout(u, nf, ph.dpn))
-        P.gmt_op_prolong_add(l, _dev(fem.to_node_layout(e, nc, ph.dpn)), ud)
+        ud = _dev(to_gpu(u, nf, ph.dpn))
+        P.gmt_op_prolong_add(l, _dev(to_gpu(e, nc, ph.dpn)), ud)
         want = u + H.P[l] @ e
-        _close(_host(ud), fem.to_node_layout(want, nf, ph.dpn),
-               fem.to_node_layout(np.abs(u) + abs(H.P[l]) @ np.abs(e), nf, ph.dpn))
+        _close(_host(ud), to_gpu(want, nf, ph.dpn),
+               to_gpu(np.abs(u) + abs(H.P[l]) @ np.abs(e), nf, ph.dpn))
 
 
 def test_vcycle_matches_oracle_and_reduction_factors(case):
@@ -197,7 +209,7 @@ def test_vcycle_matches_oracle_and_reduction_factors(case):
     for cyc in range(4):
         u = gmg.vcycle(H, u, **kw)
         P.gmt_vcycle(1)
-        ug = fem.from_node_layout(P.gmt_get_solution())
+        ug = from_gpu(P.gmt_get_solution())
         act = np.repeat(H.active[0][:, None], ph.nrhs, axis=1)
         err = np.abs(ug - u)[act].max() / np.abs(u[act]).max()
         assert err < 1e-4 * (cyc + 1), f"cycle {cyc}: rel err {err:.2e}"
@@ -233,9 +245,9 @@ def test_zero_mean_gauge(case):
     u0 = P.gmt_get_solution(zero_mean=False).astype(np.float64)
     u1 = P.gmt_get_solution(zero_mean=True).astype(np.float64)
     act_nodes = H.active[0].reshape(-1, ph.dpn)[:, 0]
-    want = gmg.project_zero_mean(fem.from_node_layout(u0), ph.dpn, act_nodes)
-    got = fem.from_node_layout(u1)
-    _close(got, want, np.abs(fem.from_node_layout(u0)).max() * np.ones_like(want), 1e-6)
+    want = gmg.project_zero_mean(from_gpu(u0), ph.dpn, act_nodes)
+    got = from_gpu(u1)
+    _close(got, want, np.abs(from_gpu(u0)).max() * np.ones_like(want), 1e-6)
 
 
 def test_alg2_injection():
@@ -249,11 +261,11 @@ def test_alg2_injection():
     u0 = 0.05 * rng.standard_normal(H.f.shape) * H.active[0][:, None]
     want = gmg.vcycle(H, u0, omega=0.45, pre=2, post=2, coarse=16, inject=inj)
     with _problem(s, kind, 3) as P:
-        P.gmt_set_initial_guess(np.ascontiguousarray(fem.to_node_layout(u0, 16, 3), dtype=np.float32))
+        P.gmt_set_initial_guess(np.ascontiguousarray(to_gpu(u0, 16, 3), dtype=np.float32))
         for l in (1, 2):
-            P.gmt_inject_correction(l, np.ascontiguousarray(fem.to_node_layout(inj[l], H.n[l], 3), dtype=np.float32))
+            P.gmt_inject_correction(l, np.ascontiguousarray(to_gpu(inj[l], H.n[l], 3), dtype=np.float32))
         P.gmt_vcycle(1)
-        got = fem.from_node_layout(P.gmt_get_solution())
+        got = from_gpu(P.gmt_get_solution())
     assert np.abs(got - want).max() <= 1e-4 * np.abs(want).max()
 
 
@@ -275,7 +287,7 @@ def test_u8_material_and_degenerate_inputs():
     H = gmg.Hierarchy(s2, ph, 1)
     with _problem(s2, "thermal", 1, coarse_sweeps=5) as P:
         P.gmt_vcycle(1)
-        got = fem.from_node_layout(P.gmt_get_solution())
+        got = from_gpu(P.gmt_get_solution())
     want = gmg.vcycle(H, np.zeros_like(H.f), omega=0.6, coarse=5)
     assert np.abs(got - want).max() <= 1e-5 * max(1e-30, np.abs(want).max())
 
