@@ -25,7 +25,7 @@
  *    node i = x + n_l (y + n_l z)).
  *  - Voigt order (11,22,33,23,13,12), engineering shear.
  *  - Inactive nodes (every incident voxel void) are outside the active set
- *    (Sec. 4.1.1): smoothing and prolongation leave them untouched.
+ *    (Sec. 4.1.1): they carry no unknowns; gmt_get_solution returns 0 there.
  *
  * Ownership: the library owns all memory it allocates; every pointer the
  * caller passes is borrowed for the duration of the call only.  Pointers

@@ -101,7 +101,11 @@ struct gmt_problem_s {
   uint8_t* u8tmp = nullptr;
   uint8_t* tflag = nullptr;   // level-0 tile activity flags (k_tile_flags)
   uint8_t* iflag = nullptr;   // level-0 interface-node flags (k_iface_flags)
+  float* code = nullptr;      // level-0 node class: uniform voxel scale, or -1 (interface)
   int* ilist = nullptr;       // sorted interface-node list (static per material)
+  int* elist = nullptr;       // sorted active-element (non-void voxel) list
+  uint8_t* eflag = nullptr;
+  int ecount = 0;
   int* icount_d = nullptr;
   int icount = 0;
   void* cub_tmp = nullptr;
@@ -205,18 +209,19 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = (ptrdiff_t)b.nodes;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
+    constexpr int NRG = 3, NG = Tr<DPN>::NR / NRG;
     const ZMap z = p->zm(0);
-    const dim3 grid(p->tntx, p->tnty, (b.nz + TT_ZC - 1) / TT_ZC), block(TT_X, TT_Y);
-    const size_t shm = (size_t)TT_NB * Tr<DPN>::V * TT_PLS * sizeof(float);
+    const dim3 grid(p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
+    const size_t shm = (size_t)TT_NB * NRG * DPN * TT_PLS * sizeof(float);
     const int nbt = grid.x * grid.y * grid.z;
     double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
     const int nbi = (p->icount + 127) / 128;
     if (mode == M_JACOBI)
-      k_fine_tiled<DPN, M_JACOBI><<<grid, block, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                            p->tflag, p->tntx, p->tnty);
+      k_fine_tiled<DPN, M_JACOBI, NRG><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                                 p->tflag, p->tntx, p->tnty);
     else
-      k_fine_tiled<DPN, M_RESID><<<grid, block, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                           p->tflag, p->tntx, p->tnty);
+      k_fine_tiled<DPN, M_RESID, NRG><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                                p->tflag, p->tntx, p->tnty);
     LAUNCHED(p);
     if (nbi > 0) {
       if (mode == M_JACOBI)
@@ -258,8 +263,9 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
   const Geo g = geo(bc.n, bc.nz);
   Prof prof(p, l == 0 ? 3 : 4);
   const float* sd = skip_void ? bc.S + (size_t)(13 * DPN * DPN) * bc.nodes : nullptr;
+  const float* actf = l == 0 ? p->code : bf.S + (size_t)(13 * DPN * DPN) * bf.nodes;
   k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
-                                                      (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes);
+                                                      (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes, actf);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -347,7 +353,7 @@ int build_operators(gmt_problem p) {
   {
     // static interface-node list (sorted, deterministic)
     const size_t total = p->lv[0].nodes;
-    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag);
+    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag, p->code);
     LAUNCHED(p);
     cub::CountingInputIterator<int> it(0);
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
@@ -356,6 +362,13 @@ int build_operators(gmt_problem p) {
     CK(cudaStreamSynchronize(st));
     if (cnt != p->icount) drop_graph(p);   // grid size of the captured interface launch changes
     p->icount = cnt;
+    // active elements (s != 0) for the C^H reduction
+    k_nonzero_flags<<<1184, 256, 0, st>>>(p->s, total, p->eflag);
+    LAUNCHED(p);
+    CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->eflag, p->elist, p->icount_d, (int)total, st));
+    CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    p->ecount = cnt;
   }
   if (L >= 2) {
     LevelBuf& b = p->lv[1];
@@ -371,8 +384,9 @@ int build_operators(gmt_problem p) {
     Prof prof(p, 6);
     if (l == 2) {
       constexpr int TE = 16;
-      k_elem_l2<DPN, TE><<<(nelem + TE - 1) / TE, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g,
-                                                                   b.Ke, b.n, b.nz);
+      const unsigned ntile = (nelem + TE - 1) / TE;
+      const unsigned grid = std::min(ntile, (unsigned)(148 * (DPN == 3 ? 1 : 16)));
+      k_elem_l2<DPN, TE><<<grid, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g, b.Ke, b.n, b.nz);
     } else {
       k_galerkin_elem<DPN><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc);
     }
@@ -405,17 +419,14 @@ int upload_material(gmt_problem p, const void* material, int dtype, int location
   return GMT_OK;
 }
 
-// Internal vectors keep zeros at inactive nodes so that void warps can skip
-// both reads and writes (k_fine / k_coarse skip_void, k_restrict): r and f
-// are only ever written by kernels that write zeros there, so clearing them
-// whenever the active set may change (new material) restores the invariant.
+// Values stored at inactive nodes never influence active ones: operator rows
+// and columns of inactive nodes are zero, restriction skips inactive fine
+// nodes and prolongation writes active fine nodes only.  Void warps therefore
+// skip reads and writes entirely, and a new material needs no buffer clearing
+// beyond resetting the solution.
 int reset_solution(gmt_problem p) {
   for (auto& b : p->lv) {
-    const size_t vb = b.nodes * p->V * sizeof(float);
-    CK(cudaMemsetAsync(b.u, 0, vb, p->stream));
-    CK(cudaMemsetAsync(b.t, 0, vb, p->stream));
-    if (b.r) CK(cudaMemsetAsync(b.r, 0, vb, p->stream));
-    if (b.f) CK(cudaMemsetAsync(b.f, 0, vb, p->stream));
+    CK(cudaMemsetAsync(b.u, 0, b.nodes * p->V * sizeof(float), p->stream));
     b.inj_pending = false;
   }
   return GMT_OK;
@@ -447,14 +458,15 @@ template <int DPN>
 int effective_tensor(gmt_problem p, const float* u, double* CH) {
   constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
   const LevelBuf& b = p->lv[0];
-  const Geo g = geo(b.n, b.nz);
+  const int nblk = std::max(1, (p->ecount + 127) / 128);
   {
     Prof prof(p, 7);
-    k_effective_tensor<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
-                                                               (float)p->ed.mu, p->part, (ptrdiff_t)b.nodes);
+    k_effective_tensor<DPN><<<nblk, 128, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
+                                                         (float)p->ed.mu, p->part, (ptrdiff_t)b.nodes, p->elist,
+                                                         p->ecount);
     LAUNCHED(p);
   }
-  TRY(reduce(p, g.nblk, NQ));
+  TRY(reduce(p, nblk, NQ));
   const double vol = (double)p->N * p->N * p->N;
   int qi = 0;
   for (int m = 0; m < NR; ++m)
@@ -474,7 +486,7 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
   // of the tiled kernel followed by those of the interface kernel
   TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
-  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) + (p->icount + 127) / 128, 2 * NR));
+  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (NR / 3) + (p->icount + 127) / 128, 2 * NR));
   for (int m = 0; m < NR; ++m) {
     const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[NR + m]);
     if (rel) rel[m] = nf > 0 ? nr_ / nf : nr_;
@@ -517,7 +529,7 @@ void free_all(gmt_problem p) {
     cudaFree(b.S); cudaFree(b.Ke); cudaFree(b.inj);
   }
   cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->M2g); cudaFree(p->tflag);
-  cudaFree(p->iflag); cudaFree(p->ilist); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  cudaFree(p->iflag); cudaFree(p->code); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
 }
@@ -634,7 +646,7 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if (l >= 2 && (rc = dalloc(p, (void**)&b.Ke, b.nodes * nd * nd * sizeof(float)))) return bail(rc);
     max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
   }
-  p->part_cap = (max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
+  p->part_cap = (2 * max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
   if ((rc = dalloc(p, (void**)&p->part, p->part_cap * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->red, 64 * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->s, (size_t)p->N * p->N * p->N * sizeof(float)))) return bail(rc);
@@ -642,7 +654,10 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   p->tnty = (cfg.res + TT_Y - 1) / TT_Y;
   if ((rc = dalloc(p, (void**)&p->tflag, (size_t)p->tntx * p->tnty * p->lv[0].nz))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->iflag, p->lv[0].nodes))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->code, p->lv[0].nodes * sizeof(float)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->ilist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->elist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->eflag, p->lv[0].nodes))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->icount_d, sizeof(int)))) return bail(rc);
   {
     cub::CountingInputIterator<int> it(0);
@@ -654,12 +669,12 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if ((rc = dalloc(p, &p->cub_tmp, bytes))) return bail(rc);
   }
   {
-    const int shm3 = TT_NB * Tr<3>::V * TT_PLS * (int)sizeof(float);
-    const int shm1 = TT_NB * Tr<1>::V * TT_PLS * (int)sizeof(float);
-    if (cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))
+    const int shm3 = TT_NB * 9 * TT_PLS * (int)sizeof(float);
+    const int shm1 = TT_NB * 3 * TT_PLS * (int)sizeof(float);
+    if (cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))
       return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
   }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);
@@ -834,6 +849,8 @@ int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) 
   const size_t vb = b.nodes * p->V * sizeof(float);
   float* dst = (location == GMT_DEVICE) ? u : b.t;   // t is scratch between cycles
   CK(cudaMemcpyAsync(dst, b.u, vb, cudaMemcpyDeviceToDevice, p->stream));
+  k_mask_inactive<<<1184, 256, 0, p->stream>>>(p->code, dst, b.nodes, p->V);   // inactive nodes -> 0
+  LAUNCHED(p);
   if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
   if (location == GMT_HOST) {
     CK(cudaMemcpyAsync(u, dst, vb, cudaMemcpyDeviceToHost, p->stream));

@@ -48,26 +48,32 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int DPN, int MODE>
+// NRG load cases per CTA (blockIdx.z = z-chunk * NG + group): the load cases
+// are independent, so splitting them halves shared memory and registers per
+// CTA and doubles the resident warps.  code[node] = uniform voxel scale of the
+// node (0 = void), or -1 for interface nodes (handled by k_iface).
+template <int DPN, int MODE, int NRG>
 __global__ void __launch_bounds__(TT_X * TT_Y)
-k_fine_tiled(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu,
-             float* __restrict__ out, int n, int nz, const FineConsts P, double* __restrict__ part,
+k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
+             float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
              ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
   using T = Tr<DPN>;
-  constexpr int NR = T::NR, V = T::V;
+  constexpr int NR = T::NR, V = NRG * DPN, NG = NR / NRG;
+  const int grp = blockIdx.z % NG, chunk = blockIdx.z / NG;
+  const float* __restrict__ u = u_all + (ptrdiff_t)grp * V * cs;
+  float* __restrict__ out = out_all + (ptrdiff_t)grp * V * cs;
   constexpr int NTH = TT_X * TT_Y;
   extern __shared__ __align__(16) float smem[];   // [TT_NB][V][TT_PY][TT_RS]
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TT_X + tx;
   const int x0 = blockIdx.x * TT_X, y0 = blockIdx.y * TT_Y;
-  const int z0 = blockIdx.z * TT_ZC, z1 = min(nz, z0 + TT_ZC);
+  const int z0 = chunk * TT_ZC, z1 = min(nz, z0 + TT_ZC);
   const int x = x0 + tx, y = y0 + ty;
   const bool valid = (x < n) && (y < n);
   const int xc = valid ? x : 0, yc = valid ? y : 0;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
-  const int xm = wrapi(xc - 1, n), ym = wrapi(yc - 1, n);
   const bool vec_rows = (x0 + TT_X <= n) && ((n & 3) == 0) && ((cs & 3) == 0);
 
   auto vflag = [&](int zv) -> bool {   // voxel-plane zv footprint non-void
@@ -119,30 +125,10 @@ k_fine_tiled(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, 
       const float* sl[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) sl[d] = smem + (size_t)((z - 1 + d + 2 * TT_NB) % TT_NB) * V * TT_PLS;
-      const int zs0 = zs(z - 1);
-      auto load_sc = [&](int qx, int qy, float(&sc)[8]) {
-        const int qxm = wrapi(qx - 1, n), qym = wrapi(qy - 1, n);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
-          sc[e] = __ldg(s + (ez ? z : zs0) * plane + (ptrdiff_t)(ey ? qy : qym) * n + (ex ? qx : qxm));
-        }
-      };
-      float sc[8];
-      if (valid) load_sc(xc, yc, sc);
-      else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sc[e] = 0.f;
-      }
-      bool act = false, uni = true;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        act |= (sc[e] != 0.f);
-        uni &= (sc[e] == sc[0]);
-      }
-      // homogeneous nodes only; interface nodes (act && !uni) belong to the
+      const float c = valid ? __ldg(code + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc) : 0.f;
+      // homogeneous nodes only; interface nodes (code -1) belong to the
       // static interface list processed by k_iface
-      if (act && uni) {
+      if (c > 0.f) {
         const int base = (ty + 1) * TT_RS + 4 + tx;
         auto get = [&](int dx, int dy, int dz, int k) -> float {
           return sl[dz + 1][k * TT_PLS + base + dy * TT_RS + dx];
@@ -150,9 +136,9 @@ k_fine_tiled(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, 
         float acc[V], fl[V], ui[V], D[DPN];
 #pragma unroll
         for (int k = 0; k < V; ++k) { fl[k] = 0.f; ui[k] = get(0, 0, 0, k); }
-        node_uniform<DPN>(get, sc[0], P.lam, P.mu, ui, acc, D);
-        op_epilogue<DPN, MODE>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, acc, fl, ui, D,
-                               P.omega, nrm, part != nullptr);
+        node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
+        op_epilogue<DPN, MODE, NRG>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, acc, fl, ui, D,
+                                    P.omega, nrm, part != nullptr, grp * NRG);
       }
     }
     __syncthreads();
@@ -166,7 +152,8 @@ k_fine_tiled(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, 
 
 // Interface nodes: those whose 8 incident voxels are not all equal (the
 // material interface).  flag = 1 per interface node (level 0).
-__global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int nz, uint8_t* __restrict__ flag) {
+__global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int nz, uint8_t* __restrict__ flag,
+                              float* __restrict__ code) {
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t total = plane * nz;
   for (ptrdiff_t i = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; i < total; i += (ptrdiff_t)gridDim.x * blockDim.x) {
@@ -180,6 +167,7 @@ __global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int n
       uni &= (__ldg(s + idx) == s0);
     }
     flag[i] = uni ? 0 : 1;
+    code[i] = uni ? s0 : -1.f;
   }
 }
 

@@ -29,17 +29,18 @@ __device__ __forceinline__ void store_node(float* __restrict__ p, ptrdiff_t cs, 
   for (int k = 0; k < Tr<DPN>::V; ++k) p[k * cs] = v[k];
 }
 
-// Common epilogue of the operator kernels.  acc = (K u)_i, fl = f_i, D = diag.
-template <int DPN, int MODE>
+// Common epilogue of the operator kernels.  acc = (K u)_i, fl = f_i, D = diag,
+// for NRG load cases starting at m0 (norm slots m0..m0+NRG-1 of 2*NR).
+template <int DPN, int MODE, int NRG = Tr<DPN>::NR>
 __device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp, ptrdiff_t cs,
-                                            const float (&acc)[Tr<DPN>::V],
-                                            const float (&fl)[Tr<DPN>::V],
-                                            const float (&ui)[Tr<DPN>::V], const float (&D)[DPN],
-                                            float omega, double (&nrm)[2 * Tr<DPN>::NR], bool want_nrm) {
-  constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
+                                            const float (&acc)[NRG * DPN], const float (&fl)[NRG * DPN],
+                                            const float (&ui)[NRG * DPN], const float (&D)[DPN],
+                                            float omega, double (&nrm)[2 * Tr<DPN>::NR], bool want_nrm,
+                                            int m0 = 0) {
+  constexpr int NR = Tr<DPN>::NR, V = NRG * DPN;
   float o[V];
 #pragma unroll
-  for (int m = 0; m < NR; ++m)
+  for (int m = 0; m < NRG; ++m)
 #pragma unroll
     for (int p = 0; p < DPN; ++p) {
       const int k = m * DPN + p;
@@ -49,11 +50,23 @@ __device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp
       else if (MODE == M_LOADS) o[k] = fl[k];
       else /* M_JACOBI */ o[k] = D[p] > 0.f ? fmaf(omega / D[p], r, ui[k]) : ui[k];
       if ((MODE == M_RESID || MODE == M_JACOBI) && want_nrm && valid) {
-        nrm[m] += (double)r * (double)r;
-        nrm[NR + m] += (double)fl[k] * (double)fl[k];
+        if (NRG == NR) {
+          nrm[m] += (double)r * (double)r;
+          nrm[NR + m] += (double)fl[k] * (double)fl[k];
+        } else {
+#pragma unroll
+          for (int mm = 0; mm < NR; ++mm)
+            if (mm == m0 + m) {
+              nrm[mm] += (double)r * (double)r;
+              nrm[NR + mm] += (double)fl[k] * (double)fl[k];
+            }
+        }
       }
     }
-  if (valid) store_node<DPN>(outp, cs, o);
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) outp[k * cs] = o[k];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -125,7 +138,7 @@ k_fine(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap z
   } else {
     if (WANT_U || MODE == M_JACOBI) load_node<DPN>(u + node, cs, ui);
     if (warp_uni) {
-      if (WANT_U) node_uniform<DPN>(get, sc[0], P.lam, P.mu, ui, acc, D);
+      if (WANT_U) node_uniform<DPN, NR>(get, sc[0], P.lam, P.mu, ui, acc, D);
       else {
 #pragma unroll
         for (int p = 0; p < DPN; ++p) {
@@ -242,12 +255,14 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
 
 // ---------------------------------------------------------------------------
 // App. E2 restriction R = P^T in gather form: coarse node I collects the 27
-// fine nodes 2I + delta with the full-weighting weights prod_d (1 - |delta_d|/2).
+// fine nodes 2I + delta with the full-weighting weights prod_d (1 - |delta_d|/2),
+// skipping inactive fine nodes (actf == 0: no stencil row exists for them),
+// so values stored at inactive nodes never matter.
 // ---------------------------------------------------------------------------
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc, int nzc, int nf,
-           const float* __restrict__ Sdiag_c, ptrdiff_t csf, ptrdiff_t csc) {
+           const float* __restrict__ Sdiag_c, ptrdiff_t csf, ptrdiff_t csc, const float* __restrict__ actf) {
   constexpr int V = Tr<DPN>::V;
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -272,6 +287,7 @@ k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc,
         const float w = (dx ? 0.5f : 1.f) * (dy ? 0.5f : 1.f) * (dz ? 0.5f : 1.f);
         const ptrdiff_t i = (ptrdiff_t)zf(2 * Z + dz) * pf + (ptrdiff_t)wrapi(2 * Y + dy, nf) * nf +
                             wrapi(2 * X + dx, nf);
+        if (actf && __ldg(actf + i) == 0.f) continue;   // R = P^T on active fine nodes only (App. E2)
         float v[V];
         load_node<DPN>(r + i, csf, v);
 #pragma unroll

@@ -25,11 +25,12 @@ __host__ __device__ constexpr bool shares(int d, int e) {
 
 // Homogeneous node (all 8 voxels at scale c): A(d) = c H(d), f = 0, in
 // difference form K u = sum_{d in half} H(d) (u_{+d} + u_{-d} - 2 u_i).
-template <int DPN, class Get>
+// NRG load cases (a group of the NR), records of NRG*DPN values.
+template <int DPN, int NRG, class Get>
 __device__ __forceinline__ void node_uniform(const Get& get, float c, float lam, float mu,
-                                             const float (&ui)[Tr<DPN>::V], float (&acc)[Tr<DPN>::V],
+                                             const float (&ui)[NRG * DPN], float (&acc)[NRG * DPN],
                                              float (&D)[DPN]) {
-  constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
+  constexpr int V = NRG * DPN;
 #pragma unroll
   for (int p = 0; p < DPN; ++p) {
     const int i = 13 * DPN * DPN + p * DPN + p;
@@ -51,7 +52,7 @@ __device__ __forceinline__ void node_uniform(const Get& get, float c, float lam,
         const int i = d * DPN * DPN + p * DPN + q;
         const float h = CT<DPN>::two ? fmaf(lam, CT<DPN>::Hl(i), mu * CT<DPN>::Hm(i)) : lam * CT<DPN>::Hl(i);
 #pragma unroll
-        for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(h, w[m * DPN + q], acc[m * DPN + p]);
+        for (int m = 0; m < NRG; ++m) acc[m * DPN + p] = fmaf(h, w[m * DPN + q], acc[m * DPN + p]);
       }
   }
 #pragma unroll

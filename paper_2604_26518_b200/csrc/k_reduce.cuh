@@ -42,21 +42,22 @@ k_reduce_stage(const double* __restrict__ part, int nblk, int nv, double* __rest
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMap zu, int n, int nz,
-                   float lam, float mu, double* __restrict__ part, ptrdiff_t cs) {
+                   float lam, float mu, double* __restrict__ part, ptrdiff_t cs,
+                   const int* __restrict__ elist, int ecount) {
   using T = Tr<DPN>;
   constexpr int NR = T::NR, V = T::V;
   constexpr int NQ = NR * (NR + 1) / 2;
   constexpr float G0 = 0.21132486540518713f;  // (1 - 1/sqrt(3)) / 2
   constexpr float G1 = 0.78867513459481287f;  // (1 + 1/sqrt(3)) / 2
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int z = blockIdx.z;
-  const bool valid = (x < n) && (y < n);
+  // thread per entry of the sorted active-element list (non-void voxels)
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   double q[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) q[k] = 0.0;
-  const float se = valid ? __ldg(s + z * plane + (ptrdiff_t)y * n + x) : 0.f;
+  const ptrdiff_t eid = it < ecount ? elist[it] : 0;
+  const int x = (int)(eid % n), y = (int)((eid / n) % n), z = (int)(eid / plane);
+  const float se = it < ecount ? __ldg(s + eid) : 0.f;
   if (se != 0.f) {
     // nodal records of the 8 corners as differences from corner 0 (exact in
     // fp32; K_e and the strains annihilate the common translation)
@@ -141,8 +142,7 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
 #pragma unroll
     for (int k = 0; k < NQ; ++k) q[k] = 0.125 * (double)se * (double)qf[k];
   }
-  const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  block_reduce_store<NQ>(q, part + (ptrdiff_t)b * NQ);
+  block_reduce_store<NQ>(q, part + (ptrdiff_t)blockIdx.x * NQ);
 }
 
 // Sum of u over active nodes per (m, c) and the active-node count (level 0).

@@ -6,10 +6,10 @@
 //   element E's Galerkin matrix is sum_j s_{2E+j} M1_j with M1_j = P_j^T K P_j
 //   (child j's unit contribution, host-computed), so no element matrices are
 //   stored at level 1.
-// Level 2 (n/4): element matrices from the level-1 elements, which are formed
-//   on the fly from the material (FROM_MATERIAL).
+// Level 2 (n/4): element matrices straight from the material through the
+//   64-matrix basis M2 (k_elem_l2).
 // Levels >= 3: element matrices from the stored level-(l-1) element matrices.
-// Element matrices are SoA: Ke[(r*ND + c) * nelem + E] (coalesced over x).
+// Element matrices are stored per element: Ke[E * ND*ND + r*ND + c].
 #pragma once
 
 #include <utility>
@@ -22,6 +22,17 @@ namespace gmt {
 struct WConsts {  // W[j][a][A] child-corner interpolation weights (App. E1)
   float W[8 * 8 * 8];
 };
+
+__global__ void k_nonzero_flags(const float* __restrict__ s, size_t n, uint8_t* __restrict__ flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    flag[i] = s[i] != 0.f ? 1 : 0;
+}
+
+__global__ void k_mask_inactive(const float* __restrict__ code, float* __restrict__ u, size_t nodes, int V) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes; i += (size_t)gridDim.x * blockDim.x)
+    if (code[i] == 0.f)
+      for (int k = 0; k < V; ++k) u[k * nodes + i] = 0.f;
+}
 
 __global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -116,9 +127,11 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
 
 // Level-2 Galerkin element matrices straight from the material:
 //   K_E = sum_{g in 4x4x4 fine voxels of E} s_g M2_g,  M2_g = P_j^T M1_i P_j
-// (g = child j's voxel i; Sec. 4.6 Eq. 17 applied twice).  One CTA per tile of
-// TE elements, one thread per matrix entry; each M2 value fetched once per
-// tile and applied to TE elements held in shared memory.
+// (g = child j's voxel i; Sec. 4.6 Eq. 17 applied twice).  Persistent CTAs of
+// ND*ND threads (thread = matrix entry t) keep their 64 basis values M2_g[t]
+// in registers and stream tiles of TE elements whose 64 voxel scales are
+// staged in shared memory.  Element matrices are stored per element:
+// Ke[E * ND*ND + t].
 template <int DPN, int TE>
 __global__ void __launch_bounds__(Tr<DPN>::ND * Tr<DPN>::ND)
 k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict__ M2,
@@ -127,41 +140,47 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
   __shared__ __align__(16) float sg[64][TE];
   const int t = threadIdx.x;
   const ptrdiff_t nelem = (ptrdiff_t)n2 * n2 * nz2;
-  const ptrdiff_t E0 = (ptrdiff_t)blockIdx.x * TE;
-  bool any = false;
-  for (int i = t; i < 64 * TE; i += NT) {
-    const int e = i % TE, g = i / TE;
-    const ptrdiff_t E = E0 + e;
-    float v = 0.f;
-    if (E < nelem) {
-      const int X = (int)(E % n2), Y = (int)((E / n2) % n2), Z = (int)(E / ((ptrdiff_t)n2 * n2));
-      const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
-      v = __ldg(s + ((ptrdiff_t)zs(4 * Z + gz) * n0 + 4 * Y + gy) * n0 + 4 * X + gx);
+  const ptrdiff_t ntile = (nelem + TE - 1) / TE;
+  float m[64];
+#pragma unroll
+  for (int g = 0; g < 64; ++g) m[g] = __ldg(M2 + g * NT + t);
+  for (ptrdiff_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const ptrdiff_t E0 = tile * TE;
+    bool any = false;
+    for (int i = t; i < 64 * TE; i += NT) {
+      const int e = i % TE, g = i / TE;
+      const ptrdiff_t E = E0 + e;
+      float v = 0.f;
+      if (E < nelem) {
+        const int X = (int)(E % n2), Y = (int)((E / n2) % n2), Z = (int)(E / ((ptrdiff_t)n2 * n2));
+        const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
+        v = __ldg(s + ((ptrdiff_t)zs(4 * Z + gz) * n0 + 4 * Y + gy) * n0 + 4 * X + gx);
+      }
+      sg[g][e] = v;
+      any |= (v != 0.f);
     }
-    sg[g][e] = v;
-    any |= (v != 0.f);
-  }
-  const bool tile_any = __syncthreads_or(any);
-  float acc[TE];
+    const bool tile_any = __syncthreads_or(any);
+    float acc[TE];
 #pragma unroll
-  for (int e = 0; e < TE; ++e) acc[e] = 0.f;
-  if (tile_any) {
-#pragma unroll 4
-    for (int g = 0; g < 64; ++g) {
-      const float m = __ldg(M2 + g * NT + t);
+    for (int e = 0; e < TE; ++e) acc[e] = 0.f;
+    if (tile_any) {
 #pragma unroll
-      for (int e = 0; e < TE; e += 4) {
-        const float4 sv = *reinterpret_cast<const float4*>(&sg[g][e]);
-        acc[e] = fmaf(sv.x, m, acc[e]);
-        acc[e + 1] = fmaf(sv.y, m, acc[e + 1]);
-        acc[e + 2] = fmaf(sv.z, m, acc[e + 2]);
-        acc[e + 3] = fmaf(sv.w, m, acc[e + 3]);
+      for (int g = 0; g < 64; ++g) {
+#pragma unroll
+        for (int e = 0; e < TE; e += 4) {
+          const float4 sv = *reinterpret_cast<const float4*>(&sg[g][e]);
+          acc[e] = fmaf(sv.x, m[g], acc[e]);
+          acc[e + 1] = fmaf(sv.y, m[g], acc[e + 1]);
+          acc[e + 2] = fmaf(sv.z, m[g], acc[e + 2]);
+          acc[e + 3] = fmaf(sv.w, m[g], acc[e + 3]);
+        }
       }
     }
-  }
 #pragma unroll
-  for (int e = 0; e < TE; ++e)
-    if (E0 + e < nelem) dst[(ptrdiff_t)t * nelem + E0 + e] = acc[e];
+    for (int e = 0; e < TE; ++e)
+      if (E0 + e < nelem) dst[(E0 + e) * NT + t] = acc[e];
+    __syncthreads();
+  }
 }
 
 // Galerkin element matrices of level lc >= 3 from the stored children:
@@ -178,13 +197,11 @@ k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, 
   const int A = r / DPN, p = r % DPN, B = c / DPN, q = c % DPN;
   const int E = blockIdx.x;
   const int X = E % nc, Y = (E / nc) % nc, Z = E / (nc * nc);
-  const ptrdiff_t nelem_c = (ptrdiff_t)nc * nc * nzc;
   const int nfr = 2 * nc;
-  const ptrdiff_t nelem_f = (ptrdiff_t)nfr * nfr * (2 * nzc);
   float acc = 0.f;
   for (int j = 0; j < 8; ++j) {
     const int cx = 2 * X + (j & 1), cy = 2 * Y + ((j >> 1) & 1), cz = 2 * Z + (j >> 2);
-    Kc[t] = __ldg(src + (ptrdiff_t)t * nelem_f + ((ptrdiff_t)cz * nfr + cy) * nfr + cx);
+    Kc[t] = __ldg(src + (((ptrdiff_t)cz * nfr + cy) * nfr + cx) * (ND * ND) + t);
     __syncthreads();
     float tv = 0.f;   // T[(a p)][(B q)], here r = (a p)
 #pragma unroll
@@ -195,7 +212,7 @@ k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, 
     for (int a = 0; a < 8; ++a) acc = fmaf(Wt.W[(j * 8 + a) * 8 + A], Tm[(a * DPN + p) * ND + c], acc);
     __syncthreads();
   }
-  dst[(ptrdiff_t)t * nelem_c + E] = acc;
+  dst[(ptrdiff_t)E * (ND * ND) + t] = acc;
 }
 
 // Assemble the 27-point block stencil of a level from its element matrices:
@@ -239,7 +256,7 @@ k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S
       for (int p = 0; p < DPN; ++p)
 #pragma unroll
         for (int q = 0; q < DPN; ++q)
-          A[p][q] += __ldg(Ke + (ptrdiff_t)((kI * DPN + p) * ND + kJ * DPN + q) * nodes + eidx[e]);
+          A[p][q] += __ldg(Ke + eidx[e] * (ND * ND) + (kI * DPN + p) * ND + kJ * DPN + q);
     }
 #pragma unroll
     for (int p = 0; p < DPN; ++p)
