@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -111,6 +112,7 @@ struct gmt_problem_s {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int tntx = 0, tnty = 0;
+  int variant = 0;            // level-0 tiled kernel: 0 scalar (3 load cases/CTA), 1 packed f32x2 pairs
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
@@ -209,19 +211,29 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = (ptrdiff_t)b.nodes;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
-    constexpr int NRG = 3, NG = Tr<DPN>::NR / NRG;
+    const bool packed = DPN == 3 && p->variant == 1;
+    const int NRG = DPN == 3 ? (packed ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
     const ZMap z = p->zm(0);
     const dim3 grid(p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
     const size_t shm = (size_t)TT_NB * NRG * DPN * TT_PLS * sizeof(float);
     const int nbt = grid.x * grid.y * grid.z;
     double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
     const int nbi = (p->icount + 127) / 128;
-    if (mode == M_JACOBI)
-      k_fine_tiled<DPN, M_JACOBI, NRG><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                                 p->tflag, p->tntx, p->tnty);
-    else
-      k_fine_tiled<DPN, M_RESID, NRG><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                                p->tflag, p->tntx, p->tnty);
+    if (packed) {
+      if (mode == M_JACOBI)
+        k_fine_tiled2<M_JACOBI><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
+                                                          p->tntx, p->tnty);
+      else
+        k_fine_tiled2<M_RESID><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
+                                                         p->tntx, p->tnty);
+    } else {
+      if (mode == M_JACOBI)
+        k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                   cs, p->tflag, p->tntx, p->tnty);
+      else
+        k_fine_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                  cs, p->tflag, p->tntx, p->tnty);
+    }
     LAUNCHED(p);
     if (nbi > 0) {
       if (mode == M_JACOBI)
@@ -486,7 +498,9 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
   // of the tiled kernel followed by those of the interface kernel
   TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
-  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (NR / 3) + (p->icount + 127) / 128, 2 * NR));
+  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (DPN == 3 ? (p->variant == 1 ? 3 : 2) : 1) +
+                    (p->icount + 127) / 128,
+             2 * NR));
   for (int m = 0; m < NR; ++m) {
     const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[NR + m]);
     if (rel) rel[m] = nf > 0 ? nr_ / nf : nr_;
@@ -669,9 +683,13 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if ((rc = dalloc(p, &p->cub_tmp, bytes))) return bail(rc);
   }
   {
+    if (const char* v = getenv("GMT_TILED_VARIANT")) p->variant = atoi(v);
+    const int shm2 = TT_NB * 6 * TT_PLS * (int)sizeof(float);
     const int shm3 = TT_NB * 9 * TT_PLS * (int)sizeof(float);
     const int shm1 = TT_NB * 3 * TT_PLS * (int)sizeof(float);
-    if (cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+    if (cudaFuncSetAttribute(k_fine_tiled2<M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
+        cudaFuncSetAttribute(k_fine_tiled2<M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))

@@ -12,11 +12,13 @@
 
 #include "gmt_common.cuh"
 #include "k_level.cuh"
+#include "f32x2.cuh"
 #include "k_op.cuh"
 
 namespace gmt {
 
 constexpr int TT_X = 32, TT_Y = 4, TT_NB = 4, TT_ZC = 16;
+constexpr int TT_AHEAD = TT_NB - 2;       // planes staged ahead of the compute (ring: z-1 .. z+NB-2)
 constexpr int TT_PY = TT_Y + 2;
 constexpr int TT_RS = 40;                 // smem row stride: halo-left at 3, interior at 4..35, halo-right at 36
 constexpr int TT_PLS = TT_PY * TT_RS;     // floats per component plane tile
@@ -76,9 +78,11 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const bool vec_rows = (x0 + TT_X <= n) && ((n & 3) == 0) && ((cs & 3) == 0);
 
-  auto vflag = [&](int zv) -> bool {   // voxel-plane zv footprint non-void
-    return flag[((ptrdiff_t)zs(zv) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
-  };
+  // tile flags of voxel planes z0-3 .. z0+ZC+1 loaded once into a bitmask
+  unsigned long long fm = 0ull;
+  for (int i = 0; i < TT_ZC + 5; ++i)
+    if (flag[((ptrdiff_t)zs(z0 - 3 + i) * nty + blockIdx.y) * ntx + blockIdx.x]) fm |= 1ull << i;
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1ull; };
   auto needed = [&](int p) -> bool {   // node plane p read by some active node of planes p-1..p+1
     return vflag(p - 2) || vflag(p - 1) || vflag(p) || vflag(p + 1);
   };
@@ -111,21 +115,25 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
 #pragma unroll
   for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
 
-  // prologue: planes z0-1, z0, z0+1
-  for (int p = z0 - 1; p <= z0 + 1; ++p) {
-    if (needed(p)) issue(p);
+  // prologue: planes z0-1 .. z0+NB-3
+  for (int p = z0 - 1; p <= z0 + TT_AHEAD - 1; ++p) {
+    if (p <= z1 && needed(p)) issue(p);
     cp_async_commit();
   }
+  const float* code_col = code + (ptrdiff_t)yc * n + xc;
+  float c_next = valid ? __ldg(code_col + (ptrdiff_t)z0 * plane) : 0.f;
   for (int z = z0; z < z1; ++z) {
-    if (z + 2 <= z1 && needed(z + 2)) issue(z + 2);
+    const float c_cur = c_next;
+    if (z + 1 < z1) c_next = valid ? __ldg(code_col + (ptrdiff_t)(z + 1) * plane) : 0.f;
+    if (z + TT_AHEAD <= z1 && needed(z + TT_AHEAD)) issue(z + TT_AHEAD);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<TT_AHEAD - 1>();
     __syncthreads();
     if (vflag(z - 1) || vflag(z)) {
       const float* sl[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) sl[d] = smem + (size_t)((z - 1 + d + 2 * TT_NB) % TT_NB) * V * TT_PLS;
-      const float c = valid ? __ldg(code + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc) : 0.f;
+      const float c = c_cur;
       // homogeneous nodes only; interface nodes (code -1) belong to the
       // static interface list processed by k_iface
       if (c > 0.f) {
@@ -139,6 +147,127 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
         node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
         op_epilogue<DPN, MODE, NRG>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, acc, fl, ui, D,
                                     P.omega, nrm, part != nullptr, grp * NRG);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
+// Elasticity variant processing load cases in pairs with packed FP32x2
+// arithmetic (FADD2/FFMA2): CTA group g handles load cases (2g, 2g+1); its
+// shared-memory slots interleave the pair, [c][row][x][2], so one LDS.64 gives
+// a packed operand.  Same algebra as node_uniform (difference form, c H(d)).
+template <int MODE>
+__global__ void __launch_bounds__(TT_X * TT_Y)
+k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
+              float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
+              ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
+  static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
+  constexpr int DPN = 3, NR = 6, NG = 3;
+  constexpr int SLOT = DPN * TT_PY * TT_RS * 2;   // floats per ring slot
+  constexpr int NTH = TT_X * TT_Y;
+  extern __shared__ __align__(16) float smem[];   // [TT_NB][c][TT_PY][TT_RS][2]
+  const int grp = blockIdx.z % NG, chunk = blockIdx.z / NG;
+  const float* __restrict__ u = u_all + (ptrdiff_t)grp * 2 * DPN * cs;   // load cases 2g, 2g+1
+  float* __restrict__ out = out_all + (ptrdiff_t)grp * 2 * DPN * cs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TT_X + tx;
+  const int x0 = blockIdx.x * TT_X, y0 = blockIdx.y * TT_Y;
+  const int z0 = chunk * TT_ZC, z1 = min(nz, z0 + TT_ZC);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = (x < n) && (y < n);
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+
+  // tile flags of voxel planes z0-3 .. z0+ZC+1 loaded once into a bitmask
+  unsigned long long fm = 0ull;
+  for (int i = 0; i < TT_ZC + 5; ++i)
+    if (flag[((ptrdiff_t)zs(z0 - 3 + i) * nty + blockIdx.y) * ntx + blockIdx.x]) fm |= 1ull << i;
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1ull; };
+  auto needed = [&](int p) -> bool { return vflag(p - 2) || vflag(p - 1) || vflag(p) || vflag(p + 1); };
+  auto issue = [&](int p) {
+    float* dst = smem + (size_t)((p + 2 * TT_NB) % TT_NB) * SLOT;
+    const float* src = u + (ptrdiff_t)zu(p) * plane;
+    constexpr int PX = TT_X + 2;
+    for (int q = tid; q < DPN * TT_PY * PX * 2; q += NTH) {
+      const int j = q & 1, r = q >> 1;
+      const int c = r / (TT_PY * PX), rem = r - c * (TT_PY * PX);
+      const int py = rem / PX, px = rem - py * PX;
+      const int gy = wrapi(y0 - 1 + py, n), gx = wrapi(x0 - 1 + px, n);
+      cp_async4(dst + ((c * TT_PY + py) * TT_RS + 3 + px) * 2 + j, src + (j * DPN + c) * cs + (ptrdiff_t)gy * n + gx);
+    }
+  };
+  // combined homogeneous stencil values h = lam Hl + mu Hm, packed (h, h);
+  // symmetry-equal entries are bit-identical, so the compiler shares them
+  auto hp = [&](int i) -> f2 {
+    const float h = fmaf(P.lam, CT<3>::Hl(i), P.mu * CT<3>::Hm(i));
+    return pk2(h, h);
+  };
+
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+  for (int p = z0 - 1; p <= z0 + TT_AHEAD - 1; ++p) {
+    if (p <= z1 && needed(p)) issue(p);
+    cp_async_commit();
+  }
+  const float* code_col = code + (ptrdiff_t)yc * n + xc;
+  float c_next = valid ? __ldg(code_col + (ptrdiff_t)z0 * plane) : 0.f;
+  for (int z = z0; z < z1; ++z) {
+    const float c_cur = c_next;
+    if (z + 1 < z1) c_next = valid ? __ldg(code_col + (ptrdiff_t)(z + 1) * plane) : 0.f;
+    if (z + TT_AHEAD <= z1 && needed(z + TT_AHEAD)) issue(z + TT_AHEAD);
+    cp_async_commit();
+    cp_async_wait<TT_AHEAD - 1>();
+    __syncthreads();
+    if (vflag(z - 1) || vflag(z)) {
+      const float c = c_cur;
+      if (c > 0.f) {
+        const float* sl[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) sl[d] = smem + (size_t)((z - 1 + d + 2 * TT_NB) % TT_NB) * SLOT;
+        const int base = ((ty + 1) * TT_RS + 4 + tx) * 2;
+        auto get2 = [&](int dx, int dy, int dz, int cc) -> f2 {
+          return *reinterpret_cast<const f2*>(sl[dz + 1] + cc * (TT_PY * TT_RS * 2) + base + (dy * TT_RS + dx) * 2);
+        };
+        f2 ui[DPN], acc[DPN];
+#pragma unroll
+        for (int cc = 0; cc < DPN; ++cc) {
+          ui[cc] = get2(0, 0, 0, cc);
+          acc[cc] = 0ull;
+        }
+#pragma unroll
+        for (int d = 14; d < 27; ++d) {
+          const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+          f2 w[DPN];
+#pragma unroll
+          for (int q = 0; q < DPN; ++q)
+            w[q] = add2(sub2(get2(dx, dy, dz, q), ui[q]), sub2(get2(-dx, -dy, -dz, q), ui[q]));
+#pragma unroll
+          for (int pp = 0; pp < DPN; ++pp)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q) {
+              if (!hom_nz(d, pp, q)) continue;
+              acc[pp] = fma2(hp(d * 9 + pp * 3 + q), w[q], acc[pp]);
+            }
+        }
+        // unpack (load case 2g, 2g+1) and reuse the scalar epilogue
+        float a[6], fl[6], uu[6], D[DPN];
+#pragma unroll
+        for (int cc = 0; cc < DPN; ++cc) {
+          upk2(mul2(acc[cc], pk2(c, c)), a[cc], a[3 + cc]);
+          upk2(ui[cc], uu[cc], uu[3 + cc]);
+          fl[cc] = fl[3 + cc] = 0.f;
+          const int i = 13 * 9 + cc * 3 + cc;
+          D[cc] = c * fmaf(P.lam, CT<3>::Hl(i), P.mu * CT<3>::Hm(i));
+        }
+        op_epilogue<DPN, MODE, 2>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, a, fl, uu, D,
+                                  P.omega, nrm, part != nullptr, grp * 2);
       }
     }
     __syncthreads();
