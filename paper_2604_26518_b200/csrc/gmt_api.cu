@@ -62,6 +62,15 @@ struct LevelBuf {
   float* S = nullptr;    // 27-point block stencil (levels >= 1)
   float* Ke = nullptr;   // Galerkin element matrices (levels >= 2)
   float* inj = nullptr;  // Alg. 2 injected correction
+  float* ecode = nullptr;  // levels >= 1: uniform scale of the element's fine voxels, or -1
+  float* ncode = nullptr;  // levels >= 1: uniform scale around the node (0 void), or -1 (interface)
+  float* Hl = nullptr;     // homogeneous 27-point block stencil of this level (device, 27*DPN*DPN)
+  float* Kh = nullptr;     // homogeneous element matrix of this level (device, ND*ND)
+  bool tiled = false;      // level >= 1 swept by the tiled kernel (uniform nodes) + interface list
+  uint8_t* tflag = nullptr;
+  int tntx = 0, tnty = 0;
+  int* ilist = nullptr;    // sorted interface nodes (ncode -1) of this coarse level
+  int icount = 0;
   bool inj_pending = false;
 };
 
@@ -95,6 +104,7 @@ struct gmt_problem_s {
   WConsts wc{};
   float* M1g = nullptr;
   float* M2g = nullptr;
+  std::vector<CoarseH> hc;    // per-level homogeneous stencil (kernel parameter)
   double* part = nullptr;
   size_t part_cap = 0;   // doubles
   double* red = nullptr; // device reduction results
@@ -255,13 +265,30 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
       case M_DIAG: k_fine<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(p->s, z, u, z, f, out, b.n, b.nz, p->fc, part, skip_void, cs); break;
       default: return fail(GMT_ERR_ARG, "bad mode");
     }
+  } else if (b.tiled && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
+    const ZMap z = p->zm(l);
+    const dim3 grid(b.tntx, b.tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * (Tr<DPN>::NR / 3)), block(TT_X, TT_Y);
+    const size_t shm = (size_t)TT_NB * 3 * DPN * TT_PLS * sizeof(float);
+    if (mode == M_JACOBI)
+      k_fine_tiled<DPN, M_JACOBI, 3, true><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, p->fc, nullptr,
+                                                                     cs, b.tflag, b.tntx, b.tnty, f, p->hc[l]);
+    else
+      k_fine_tiled<DPN, M_RESID, 3, true><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, p->fc, nullptr,
+                                                                    cs, b.tflag, b.tntx, b.tnty, f, p->hc[l]);
+    LAUNCHED(p);
+    if (b.icount == 0) return GMT_OK;
+    const int nbi = (b.icount + 127) / 128;
+    if (mode == M_JACOBI)
+      k_coarse_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+    else
+      k_coarse_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
   } else {
     const ZMap z = p->zm(l);
     switch (mode) {
-      case M_APPLY: k_coarse<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
-      case M_RESID: k_coarse<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
-      case M_JACOBI: k_coarse<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
-      case M_DIAG: k_coarse<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs); break;
+      case M_APPLY: k_coarse<DPN, M_APPLY><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs, b.ncode, p->hc[l]); break;
+      case M_RESID: k_coarse<DPN, M_RESID><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs, b.ncode, p->hc[l]); break;
+      case M_JACOBI: k_coarse<DPN, M_JACOBI><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs, b.ncode, p->hc[l]); break;
+      case M_DIAG: k_coarse<DPN, M_DIAG><<<g.grid, g.block, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, part, skip_void, cs, b.ncode, p->hc[l]); break;
       default: return fail(GMT_ERR_ARG, "bad mode");
     }
   }
@@ -274,8 +301,8 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
   const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
   const Geo g = geo(bc.n, bc.nz);
   Prof prof(p, l == 0 ? 3 : 4);
-  const float* sd = skip_void ? bc.S + (size_t)(13 * DPN * DPN) * bc.nodes : nullptr;
-  const float* actf = l == 0 ? p->code : bf.S + (size_t)(13 * DPN * DPN) * bf.nodes;
+  const float* sd = skip_void ? bc.ncode : nullptr;
+  const float* actf = l == 0 ? p->code : bf.ncode;
   k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
                                                       (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes, actf);
   LAUNCHED(p);
@@ -293,8 +320,8 @@ int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
                                                                  (ptrdiff_t)bc.nodes);
   else
     k_prolong_add<DPN, false><<<g.grid, g.block, 0, p->stream>>>(
-        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0),
-        bf.S + (size_t)(13 * DPN * DPN) * bf.nodes, (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes);
+        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0), bf.ncode, (ptrdiff_t)bf.nodes,
+        (ptrdiff_t)bc.nodes);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -320,7 +347,7 @@ int coarsest(gmt_problem p) {
   const int sweeps = p->cfg.coarse_sweeps;
   if (l == 0 || b.nodes > 32768) return smooth<DPN>(p, l, sweeps);
   Prof prof(p, 5);
-  k_coarsest<DPN><<<1, 1024, 0, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps, (float)p->cfg.omega);
+  k_coarsest<DPN><<<1, 1024, 0, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps, (float)p->cfg.omega, b.ncode, b.Hl);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -383,11 +410,37 @@ int build_operators(gmt_problem p) {
     p->ecount = cnt;
   }
   if (L >= 2) {
+    // homogeneity pyramid: element / node codes of every coarse level
+    LevelBuf& b1 = p->lv[1];
+    k_elem_code_l1<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b1.ecode, b1.n, b1.nz);
+    LAUNCHED(p);
+    for (int l = 1; l < L; ++l) {
+      LevelBuf& b = p->lv[l];
+      if (l >= 2) {
+        k_elem_code_up<<<1184, 256, 0, st>>>(p->lv[l - 1].ecode, p->lv[l - 1].n, b.ecode, b.n, b.nz);
+        LAUNCHED(p);
+      }
+      k_node_code<<<1184, 256, 0, st>>>(b.ecode, p->zm(l), b.ncode, b.n, b.nz);
+      LAUNCHED(p);
+      if (b.tiled) {
+        k_tile_flags<<<dim3(b.tntx, b.tnty, b.nz), 128, 0, st>>>(b.ecode, p->zm(l), b.n, b.nz, b.tntx, b.tnty, b.tflag);
+        LAUNCHED(p);
+        k_neg_flags<<<1184, 256, 0, st>>>(b.ncode, b.nodes, p->iflag);
+        LAUNCHED(p);
+        cub::CountingInputIterator<int> it(0);
+        CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, b.ilist, p->icount_d, (int)b.nodes, st));
+        int cnt = 0;
+        CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (cnt != b.icount) drop_graph(p);
+        b.icount = cnt;
+      }
+    }
     LevelBuf& b = p->lv[1];
     const Geo g = geo(b.n, b.nz);
     Prof prof(p, 6);
     k_stencil_l1<DPN><<<g.grid, g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz,
-                                                  (float)p->ed.lam, (float)p->ed.mu);
+                                                  (float)p->ed.lam, (float)p->ed.mu, b.ncode);
     LAUNCHED(p);
   }
   for (int l = 2; l < L; ++l) {
@@ -398,13 +451,14 @@ int build_operators(gmt_problem p) {
       constexpr int TE = 16;
       const unsigned ntile = (nelem + TE - 1) / TE;
       const unsigned grid = std::min(ntile, (unsigned)(148 * (DPN == 3 ? 1 : 16)));
-      k_elem_l2<DPN, TE><<<grid, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g, b.Ke, b.n, b.nz);
+      k_elem_l2<DPN, TE><<<grid, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g, b.Ke, b.n, b.nz, b.ecode);
     } else {
-      k_galerkin_elem<DPN><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc);
+      k_galerkin_elem<DPN><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc, p->lv[l - 1].ecode,
+                                                     b.ecode, p->lv[l - 1].Kh);
     }
     LAUNCHED(p);
     const Geo g = geo(b.n, b.nz);
-    k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz);
+    k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode, b.ncode, b.Kh);
     LAUNCHED(p);
   }
   return GMT_OK;
@@ -541,6 +595,7 @@ void free_all(gmt_problem p) {
   for (auto& b : p->lv) {
     cudaFree(b.u); cudaFree(b.t); cudaFree(b.f); cudaFree(b.r);
     cudaFree(b.S); cudaFree(b.Ke); cudaFree(b.inj);
+    cudaFree(b.ecode); cudaFree(b.ncode); cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.tflag); cudaFree(b.ilist);
   }
   cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->M2g); cudaFree(p->tflag);
   cudaFree(p->iflag); cudaFree(p->code); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
@@ -646,6 +701,9 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   }
   p->lv.resize(L);
   const size_t V = p->V;
+  // coarse levels at least this fine use the tiled sweep (env override for tests)
+  int coarse_tiled_min = 64;
+  if (const char* v = getenv("GMT_COARSE_TILED_MIN")) coarse_tiled_min = std::max(2, atoi(v));
   size_t max_blk = 0;
   for (int l = 0; l < L; ++l) {
     LevelBuf& b = p->lv[l];
@@ -658,6 +716,19 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if ((l < L - 1 || l == 0) && (rc = dalloc(p, (void**)&b.r, vb))) return bail(rc);
     if (l >= 1 && (rc = dalloc(p, (void**)&b.S, b.nodes * 27 * p->dpn * p->dpn * sizeof(float)))) return bail(rc);
     if (l >= 2 && (rc = dalloc(p, (void**)&b.Ke, b.nodes * nd * nd * sizeof(float)))) return bail(rc);
+    if (l >= 1 && ((rc = dalloc(p, (void**)&b.ecode, b.nodes * sizeof(float))) ||
+                   (rc = dalloc(p, (void**)&b.ncode, b.nodes * sizeof(float)))))
+      return bail(rc);
+    if ((rc = dalloc(p, (void**)&b.Hl, 27 * 9 * sizeof(float))) || (rc = dalloc(p, (void**)&b.Kh, 576 * sizeof(float))))
+      return bail(rc);
+    b.tiled = l >= 1 && l < L - 1 && b.n >= coarse_tiled_min;
+    if (b.tiled) {
+      b.tntx = (b.n + TT_X - 1) / TT_X;
+      b.tnty = (b.n + TT_Y - 1) / TT_Y;
+      if ((rc = dalloc(p, (void**)&b.tflag, (size_t)b.tntx * b.tnty * b.nz)) ||
+          (rc = dalloc(p, (void**)&b.ilist, b.nodes * sizeof(int))))
+        return bail(rc);
+    }
     max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
   }
   p->part_cap = (2 * max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
@@ -690,6 +761,10 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     if (cudaFuncSetAttribute(k_fine_tiled2<M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled2<M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))
@@ -708,6 +783,28 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     return bail(fail(GMT_ERR_NOMEM, "cudaMallocHost failed"));
   if (cudaMemcpy(p->M1g, m1.data(), 8 * nd * nd * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
     return bail(fail(GMT_ERR_CUDA, "M1 upload failed"));
+  {
+    std::vector<double> kh((size_t)L * 576), hh((size_t)L * 243);
+    homogeneous_levels(p->ed, L, reinterpret_cast<double(*)[576]>(kh.data()),
+                       reinterpret_cast<double(*)[243]>(hh.data()));
+    std::vector<float> khf(576), hhf(243);
+    for (int l = 0; l < L; ++l) {
+      for (int i = 0; i < 576; ++i) khf[i] = (float)kh[(size_t)l * 576 + i];
+      for (int i = 0; i < 243; ++i) hhf[i] = (float)hh[(size_t)l * 243 + i];
+      p->hc.resize(L);
+      for (int i = 0; i < 243; ++i) p->hc[l].H[i] = hhf[i];
+      if (cudaMemcpy(p->lv[l].Kh, khf.data(), 576 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(p->lv[l].Hl, hhf.data(), 243 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(GMT_ERR_CUDA, "homogeneous table upload failed"));
+    }
+  }
+  // zero every vector once: values at inactive nodes are never read except as
+  // (zero-coefficient) neighbours, so they must be finite
+  for (auto& b : p->lv) {
+    const size_t vb = b.nodes * p->V * sizeof(float);
+    for (float* v : {b.u, b.t, b.f, b.r})
+      if (v && cudaMemsetAsync(v, 0, vb, p->stream) != cudaSuccess) return bail(fail(GMT_ERR_CUDA, "memset failed"));
+  }
   if ((rc = upload_material(p, material, material_dtype, material_location))) return bail(rc);
   if ((rc = rebuild(p))) return bail(rc);
   if (cudaStreamSynchronize(p->stream) != cudaSuccess) {
@@ -964,8 +1061,8 @@ int gmt_op_stencil(gmt_problem p, int level, float* S) {
   if (!S) return fail(GMT_ERR_ARG, "null output");
   TRY(set_device(p));
   const LevelBuf& b = p->lv[level];
-  CK(cudaMemcpyAsync(S, b.S, b.nodes * 27 * p->dpn * p->dpn * sizeof(float), cudaMemcpyDeviceToDevice,
-                     p->stream));
+  k_expand_stencil<<<1184, 256, 0, p->stream>>>(b.ncode, b.S, b.Hl, S, b.nodes, 27 * p->dpn * p->dpn);
+  LAUNCHED(p);
   return GMT_OK;
 }
 

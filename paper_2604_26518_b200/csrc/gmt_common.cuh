@@ -30,6 +30,10 @@ __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >
 
 // Kernel parameter blocks: element constants live in the param constant bank,
 // so fully unrolled loops issue FFMA with c[0x0][imm] operands.
+struct CoarseH {         // homogeneous Galerkin stencil of one coarse level (c H_l at uniform nodes)
+  float H[27 * 9];
+};
+
 struct FineConsts {      // level 0 (material-driven) operator: material scalars
   float lam, mu;         // Lame constants (elastic) / kappa in lam (heat)
   float omega;           // damped-Jacobi factor

@@ -189,4 +189,46 @@ bool build_element_data_lm(int physics, double lam, double mu, double kappa, Ele
   return true;
 }
 
+void homogeneous_levels(const ElementData& ed, int levels, double (*Khom)[24 * 24], double (*Hhom)[27 * 9]) {
+  const int dpn = ed.dpn, nd = ed.nd;
+  for (int i = 0; i < nd * nd; ++i) Khom[0][i] = ed.K[i];
+  for (int l = 1; l < levels; ++l)
+    for (int A = 0; A < 8; ++A)
+      for (int B = 0; B < 8; ++B)
+        for (int p = 0; p < dpn; ++p)
+          for (int q = 0; q < dpn; ++q) {
+            double acc = 0.0;
+            for (int j = 0; j < 8; ++j)
+              for (int a = 0; a < 8; ++a) {
+                const double wa = ed.W[j][a][A];
+                if (wa == 0.0) continue;
+                for (int b = 0; b < 8; ++b) {
+                  const double wb = ed.W[j][b][B];
+                  if (wb == 0.0) continue;
+                  acc += wa * wb * Khom[l - 1][(a * dpn + p) * nd + b * dpn + q];
+                }
+              }
+            Khom[l][(A * dpn + p) * nd + B * dpn + q] = acc;
+          }
+  for (int l = 0; l < levels; ++l)
+    for (int d = 0; d < 27; ++d) {
+      const int dd[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+      for (int p = 0; p < dpn; ++p)
+        for (int q = 0; q < dpn; ++q) {
+          double acc = 0.0;
+          for (int e = 0; e < 8; ++e) {
+            const int ee[3] = {e & 1, (e >> 1) & 1, e >> 2};
+            bool shared = true;
+            for (int a = 0; a < 3; ++a)
+              if ((dd[a] == -1 && ee[a]) || (dd[a] == 1 && !ee[a])) shared = false;
+            if (!shared) continue;
+            const int ki = (1 - ee[0]) + 2 * (1 - ee[1]) + 4 * (1 - ee[2]);
+            const int kj = ki + dd[0] + 2 * dd[1] + 4 * dd[2];
+            acc += Khom[l][(ki * dpn + p) * nd + kj * dpn + q];
+          }
+          Hhom[l][(d * dpn + p) * dpn + q] = acc;
+        }
+    }
+}
+
 }  // namespace gmt

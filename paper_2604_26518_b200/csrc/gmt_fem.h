@@ -24,6 +24,12 @@ struct ElementData {
   double lam, mu;         // Lame constants (elastic) / kappa in lam (thermal)
 };
 
+// Homogeneous Galerkin hierarchy: element matrix of a level-l element whose
+// fine voxels all have scale 1, Khom[1] = sum_j M1_j and Khom[l+1] =
+// sum_j P_j^T Khom[l] P_j (Sec. 4.6 Eq. 17), and its assembled 27-point block
+// stencil Hhom[l][d][p][q].  Level 0 is the unit element itself.
+void homogeneous_levels(const ElementData& ed, int levels, double (*Khom)[24 * 24], double (*Hhom)[27 * 9]);
+
 // physics: 0 elastic (E, nu), 1 thermal (kappa).  Returns false on bad input.
 bool build_element_data(int physics, double E, double nu, double kappa, ElementData* out);
 // Same from Lame constants (elastic) / kappa (thermal) without range checks;

@@ -54,11 +54,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // are independent, so splitting them halves shared memory and registers per
 // CTA and doubles the resident warps.  code[node] = uniform voxel scale of the
 // node (0 = void), or -1 for interface nodes (handled by k_iface).
-template <int DPN, int MODE, int NRG>
+// COARSE: level >= 1 -- uniform nodes use c H_l from the kernel parameter HP
+// (direct form; coarse vectors are corrections), and the right-hand side f is
+// read from memory (the restricted residual) instead of being zero.
+template <int DPN, int MODE, int NRG, bool COARSE = false>
 __global__ void __launch_bounds__(TT_X * TT_Y)
 k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
              float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
-             ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
+             ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty,
+             const float* __restrict__ f_all = nullptr, const CoarseH HP = CoarseH{}) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
   using T = Tr<DPN>;
   constexpr int NR = T::NR, V = NRG * DPN, NG = NR / NRG;
@@ -144,9 +148,38 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
         float acc[V], fl[V], ui[V], D[DPN];
 #pragma unroll
         for (int k = 0; k < V; ++k) { fl[k] = 0.f; ui[k] = get(0, 0, 0, k); }
-        node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
-        op_epilogue<DPN, MODE, NRG>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, acc, fl, ui, D,
-                                    P.omega, nrm, part != nullptr, grp * NRG);
+        const ptrdiff_t node = (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc;
+        if constexpr (COARSE) {
+#pragma unroll
+          for (int p = 0; p < DPN; ++p) D[p] = c * HP.H[(13 * DPN + p) * DPN + p];
+#pragma unroll
+          for (int m = 0; m < NRG; ++m)
+#pragma unroll
+            for (int p = 0; p < DPN; ++p) acc[m * DPN + p] = HP.H[(13 * DPN + p) * DPN + p] * ui[m * DPN + p];
+#pragma unroll
+          for (int d = 14; d < 27; ++d) {
+            const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+            float w[V];
+#pragma unroll
+            for (int k = 0; k < V; ++k) w[k] = get(dx, dy, dz, k) + get(-dx, -dy, -dz, k);
+#pragma unroll
+            for (int p = 0; p < DPN; ++p)
+#pragma unroll
+              for (int q = 0; q < DPN; ++q) {
+                const float h = HP.H[(d * DPN + p) * DPN + q];
+#pragma unroll
+                for (int m = 0; m < NRG; ++m) acc[m * DPN + p] = fmaf(h, w[m * DPN + q], acc[m * DPN + p]);
+              }
+          }
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc[k] *= c;
+          const float* f = f_all + (ptrdiff_t)grp * V * cs;
+#pragma unroll
+          for (int k = 0; k < V; ++k) fl[k] = __ldg(f + k * cs + node);
+        } else {
+          node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
+        }
+        op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr, grp * NRG);
       }
     }
     __syncthreads();
@@ -298,6 +331,41 @@ __global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int n
     flag[i] = uni ? 0 : 1;
     code[i] = uni ? s0 : -1.f;
   }
+}
+
+// Coarse-level interface nodes (ncode -1) from a sorted list: stored
+// Galerkin stencil, f from memory.
+template <int DPN, int MODE>
+__global__ void __launch_bounds__(128)
+k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu, const float* __restrict__ f,
+               float* __restrict__ out, int n, int nz, float omega, ptrdiff_t cs, const int* __restrict__ list,
+               int count) {
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = T::V;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const ptrdiff_t plane = (ptrdiff_t)n * n, nodes = plane * nz;
+  const ptrdiff_t node = list[i];
+  const int x = (int)(node % n), y = (int)((node / n) % n), z = (int)(node / plane);
+  float acc[V], fl[V], ui[V], D[DPN];
+#pragma unroll
+  for (int k = 0; k < V; ++k) { acc[k] = 0.f; ui[k] = __ldg(u + k * cs + node); fl[k] = __ldg(f + k * cs + node); }
+#pragma unroll
+  for (int d = 0; d < 27; ++d) {
+    const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+    const ptrdiff_t j = (ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(y + dy, n) * n + wrapi(x + dx, n);
+#pragma unroll
+    for (int p = 0; p < DPN; ++p)
+#pragma unroll
+      for (int q = 0; q < DPN; ++q) {
+        const float a = __ldg(S + (ptrdiff_t)((d * DPN + p) * DPN + q) * nodes + node);
+        if (d == 13 && p == q) D[p] = a;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, __ldg(u + (m * DPN + q) * cs + j), acc[m * DPN + p]);
+      }
+  }
+  double nrm[2 * NR];
+  op_epilogue<DPN, MODE>(true, out + node, cs, acc, fl, ui, D, omega, nrm, false);
 }
 
 // The general (interface) path over the static interface-node list.

@@ -177,7 +177,8 @@ template <int DPN, int MODE>
 __global__ void __launch_bounds__(128)
 k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
          const float* __restrict__ f, float* __restrict__ out, int n, int nz, float omega,
-         double* __restrict__ part, int skip_void, ptrdiff_t cs) {
+         double* __restrict__ part, int skip_void, ptrdiff_t cs, const float* __restrict__ ncd,
+         const CoarseH HP) {
   using T = Tr<DPN>;
   constexpr int NR = T::NR, V = T::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -189,12 +190,16 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
   const ptrdiff_t nodes = plane * nz;
   const ptrdiff_t node = z * plane + (ptrdiff_t)yc * n + xc;
 
+  // homogeneity pyramid: uniform nodes use c H_l, interface nodes (c = -1)
+  // their stored Galerkin stencil, void nodes (c = 0) are inactive
+  const float c = valid ? __ldg(ncd + node) : 0.f;
   float D[DPN];
 #pragma unroll
-  for (int p = 0; p < DPN; ++p) D[p] = valid ? __ldg(S + ((13 * DPN + p) * DPN + p) * nodes + node) : 0.f;
-  bool act = false;
-#pragma unroll
-  for (int p = 0; p < DPN; ++p) act |= (D[p] != 0.f);
+  for (int p = 0; p < DPN; ++p) {
+    const int k = (13 * DPN + p) * DPN + p;
+    D[p] = c >= 0.f ? c * HP.H[k] : __ldg(S + (ptrdiff_t)k * nodes + node);
+  }
+  const bool act = c != 0.f;
 
   float acc[V], fl[V], ui[V];
 #pragma unroll
@@ -207,30 +212,61 @@ k_coarse(const float* __restrict__ S, const float* __restrict__ u, ZMap zu,
   const bool do_write = warp_act || !skip_void;
   if (warp_act) {
     if (MODE != M_DIAG && MODE != M_LOADS) {
+      load_node<DPN>(u + node, cs, ui);
+      auto nbp = [&](int dx, int dy, int dz) -> const float* {
+        return u + ((ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(yc + dy, n) * n + wrapi(xc + dx, n));
+      };
+      if (c > 0.f) {
+        // uniform node: c H_l, symmetric pairs H_l(-d) = H_l(d)
 #pragma unroll
-      for (int d = 0; d < 27; ++d) {
-        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
-        float A[DPN][DPN];
+        for (int m = 0; m < NR; ++m)
 #pragma unroll
-        for (int p = 0; p < DPN; ++p)
+          for (int p = 0; p < DPN; ++p) acc[m * DPN + p] = HP.H[(13 * DPN + p) * DPN + p] * ui[m * DPN + p];
 #pragma unroll
-          for (int q = 0; q < DPN; ++q)
-            A[p][q] = valid ? __ldg(S + ((d * DPN + p) * DPN + q) * nodes + node) : 0.f;
-        float uj[V];
-        load_node<DPN>(u + ((ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(yc + dy, n) * n +
-                            wrapi(xc + dx, n)), cs, uj);
-        if (d == 13) {
+        for (int d = 14; d < 27; ++d) {
+          const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+          float w[V], v[V];
+          load_node<DPN>(nbp(dx, dy, dz), cs, w);
+          load_node<DPN>(nbp(-dx, -dy, -dz), cs, v);
 #pragma unroll
-          for (int k = 0; k < V; ++k) ui[k] = uj[k];
+          for (int k = 0; k < V; ++k) w[k] += v[k];
+#pragma unroll
+          for (int p = 0; p < DPN; ++p)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q) {
+              const float h = HP.H[(d * DPN + p) * DPN + q];
+#pragma unroll
+              for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(h, w[m * DPN + q], acc[m * DPN + p]);
+            }
         }
 #pragma unroll
-        for (int p = 0; p < DPN; ++p)
+        for (int k = 0; k < V; ++k) acc[k] *= c;
+      } else if (c < 0.f) {
+        // interface node: stored Galerkin stencil
 #pragma unroll
-          for (int q = 0; q < DPN; ++q) {
-            const float a = A[p][q];
+        for (int d = 0; d < 27; ++d) {
+          const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+          float A[DPN][DPN];
 #pragma unroll
-            for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, uj[m * DPN + q], acc[m * DPN + p]);
+          for (int p = 0; p < DPN; ++p)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q) A[p][q] = __ldg(S + (ptrdiff_t)((d * DPN + p) * DPN + q) * nodes + node);
+          float uj[V];
+          if (d == 13) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) uj[k] = ui[k];
+          } else {
+            load_node<DPN>(nbp(dx, dy, dz), cs, uj);
           }
+#pragma unroll
+          for (int p = 0; p < DPN; ++p)
+#pragma unroll
+            for (int q = 0; q < DPN; ++q) {
+              const float a = A[p][q];
+#pragma unroll
+              for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, uj[m * DPN + q], acc[m * DPN + p]);
+            }
+        }
       }
     }
   } else if (MODE == M_JACOBI && do_write) {
@@ -270,7 +306,7 @@ k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc,
   const bool valid = X < nc && Y < nc;
   if (Sdiag_c) {
     // skip warps of inactive coarse nodes (f_c stays 0 there: R r = 0)
-    const bool act = valid && __ldg(Sdiag_c + ((ptrdiff_t)Z * nc + Y) * nc + X) != 0.f;
+    const bool act = valid && __ldg(Sdiag_c + ((ptrdiff_t)Z * nc + Y) * nc + X) != 0.f;   // coarse node code
     if (!__any_sync(0xffffffffu, act)) return;
   }
   if (!valid) return;
@@ -355,7 +391,7 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
 template <int DPN>
 __global__ void __launch_bounds__(1024)
 k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, float* t, int n,
-           int sweeps, float omega) {
+           int sweeps, float omega, const float* __restrict__ ncd, const float* __restrict__ Hl) {
   constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V;
   const int nodes = n * n * n;
   for (int it = 0; it < sweeps; ++it) {
@@ -370,10 +406,14 @@ k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, f
         const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
         const int j = (wrapi(z + dz, n) * n + wrapi(y + dy, n)) * n + wrapi(x + dx, n);
         float A[DPN][DPN];
+        const float c = ncd[i];
 #pragma unroll
         for (int p = 0; p < DPN; ++p)
 #pragma unroll
-          for (int q = 0; q < DPN; ++q) A[p][q] = S[((d * DPN + p) * DPN + q) * nodes + i];
+          for (int q = 0; q < DPN; ++q) {
+            const int k = (d * DPN + p) * DPN + q;
+            A[p][q] = c >= 0.f ? c * Hl[k] : S[k * nodes + i];
+          }
 #pragma unroll
         for (int m = 0; m < NR; ++m)
 #pragma unroll
@@ -387,7 +427,8 @@ k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, f
 #pragma unroll
         for (int p = 0; p < DPN; ++p) {
           const int k = m * DPN + p;
-          const float Dp = S[((13 * DPN + p) * DPN + p) * nodes + i];
+          const int kd = (13 * DPN + p) * DPN + p;
+          const float Dp = ncd[i] >= 0.f ? ncd[i] * Hl[kd] : S[kd * nodes + i];
           const float ui = src[k * nodes + i];
           dst[k * nodes + i] = Dp > 0.f ? fmaf(omega / Dp, f[k * nodes + i] - acc[k], ui) : ui;
         }

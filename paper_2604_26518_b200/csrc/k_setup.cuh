@@ -23,6 +23,71 @@ struct WConsts {  // W[j][a][A] child-corner interpolation weights (App. E1)
   float W[8 * 8 * 8];
 };
 
+// ---- homogeneity pyramid (levels >= 1) ---------------------------------------
+// ecode: uniform voxel scale of all fine voxels inside a coarse element, or -1.
+// ncode: uniform scale of all voxels under the 8 elements around a node
+// (0 = void / inactive), or -1 (interface: the node needs its stored stencil).
+__global__ void k_elem_code_l1(const float* __restrict__ s, ZMap zs, int n0, float* __restrict__ ec, int n1,
+                               int nz1) {
+  const ptrdiff_t total = (ptrdiff_t)n1 * n1 * nz1;
+  for (ptrdiff_t E = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; E < total; E += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const int X = (int)(E % n1), Y = (int)((E / n1) % n1), Z = (int)(E / ((ptrdiff_t)n1 * n1));
+    float v0 = 0.f;
+    bool uni = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float v = __ldg(s + ((ptrdiff_t)zs(2 * Z + (j >> 2)) * n0 + 2 * Y + ((j >> 1) & 1)) * n0 + 2 * X + (j & 1));
+      if (j == 0) v0 = v; else uni &= (v == v0);
+    }
+    ec[E] = uni ? v0 : -1.f;
+  }
+}
+
+__global__ void k_elem_code_up(const float* __restrict__ ecf, int nf, float* __restrict__ ecc, int nc, int nzc) {
+  const ptrdiff_t total = (ptrdiff_t)nc * nc * nzc;
+  for (ptrdiff_t E = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; E < total; E += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const int X = (int)(E % nc), Y = (int)((E / nc) % nc), Z = (int)(E / ((ptrdiff_t)nc * nc));
+    float v0 = 0.f;
+    bool uni = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float v = __ldg(ecf + ((ptrdiff_t)(2 * Z + (j >> 2)) * nf + 2 * Y + ((j >> 1) & 1)) * nf + 2 * X + (j & 1));
+      if (j == 0) v0 = v; else uni &= (v == v0);
+    }
+    ecc[E] = (uni && v0 >= 0.f) ? v0 : -1.f;
+  }
+}
+
+__global__ void k_node_code(const float* __restrict__ ec, ZMap ze, float* __restrict__ ncd, int n, int nz) {
+  const ptrdiff_t plane = (ptrdiff_t)n * n, total = plane * nz;
+  for (ptrdiff_t i = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; i < total; i += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const int X = (int)(i % n), Y = (int)((i / n) % n), Z = (int)(i / plane);
+    const int xm = wrapi(X - 1, n), ym = wrapi(Y - 1, n), zm = ze(Z - 1);
+    float v0 = 0.f;
+    bool uni = true;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = __ldg(ec + ((e >> 2) ? Z : zm) * plane + (ptrdiff_t)(((e >> 1) & 1) ? Y : ym) * n + ((e & 1) ? X : xm));
+      if (e == 0) v0 = v; else uni &= (v == v0);
+    }
+    ncd[i] = (uni && v0 >= 0.f) ? v0 : -1.f;
+  }
+}
+
+// Full stencil of a level for the row-level API: c H_l at uniform nodes.
+__global__ void k_expand_stencil(const float* __restrict__ ncd, const float* __restrict__ S,
+                                 const float* __restrict__ Hl, float* __restrict__ out, size_t nodes, int ns) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes; i += (size_t)gridDim.x * blockDim.x) {
+    const float c = ncd[i];
+    for (int k = 0; k < ns; ++k) out[k * nodes + i] = c >= 0.f ? c * Hl[k] : S[k * nodes + i];
+  }
+}
+
+__global__ void k_neg_flags(const float* __restrict__ c, size_t n, uint8_t* __restrict__ flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    flag[i] = c[i] < 0.f ? 1 : 0;
+}
+
 __global__ void k_nonzero_flags(const float* __restrict__ s, size_t n, uint8_t* __restrict__ flag) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     flag[i] = s[i] != 0.f ? 1 : 0;
@@ -91,37 +156,26 @@ __device__ __forceinline__ void l1_all(std::integer_sequence<int, Ds...>, const 
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc,
-             float lam, float mu) {
+             float lam, float mu, const float* __restrict__ ncd) {
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
   const int Z = blockIdx.z;
-  const bool valid = X < nc && Y < nc;
-  const int Xc = valid ? X : 0, Yc = valid ? Y : 0;
+  if (X >= nc || Y >= nc) return;
+  const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
+  const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
+  if (__ldg(ncd + node) >= 0.f) return;        // uniform / void node: c H_1, nothing stored
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   float sv[64];
-  bool any = false;
 #pragma unroll
   for (int fz = 0; fz < 4; ++fz) {
     const ptrdiff_t zo = (ptrdiff_t)zs(2 * Z - 2 + fz) * pf;
 #pragma unroll
     for (int fy = 0; fy < 4; ++fy) {
-      const ptrdiff_t yo = zo + (ptrdiff_t)wrapi(2 * Yc - 2 + fy, nf) * nf;
+      const ptrdiff_t yo = zo + (ptrdiff_t)wrapi(2 * Y - 2 + fy, nf) * nf;
 #pragma unroll
-      for (int fx = 0; fx < 4; ++fx) {
-        const float v = __ldg(s + yo + wrapi(2 * Xc - 2 + fx, nf));
-        sv[(fz * 4 + fy) * 4 + fx] = v;
-        any |= (v != 0.f);
-      }
+      for (int fx = 0; fx < 4; ++fx) sv[(fz * 4 + fy) * 4 + fx] = __ldg(s + yo + wrapi(2 * X - 2 + fx, nf));
     }
   }
-  const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
-  const ptrdiff_t node = ((ptrdiff_t)Z * nc + Yc) * nc + Xc;
-  if (!__any_sync(0xffffffffu, any)) {       // void warp: all-zero stencil
-    if (valid)
-      for (int k = 0; k < 27 * DPN * DPN; ++k) S[k * nodes + node] = 0.f;
-    return;
-  }
-  if (!valid) return;
   l1_all<DPN>(std::make_integer_sequence<int, 27>{}, sv, lam, mu, S, nodes, node);
 }
 
@@ -135,7 +189,7 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
 template <int DPN, int TE>
 __global__ void __launch_bounds__(Tr<DPN>::ND * Tr<DPN>::ND)
 k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict__ M2,
-          float* __restrict__ dst, int n2, int nz2) {
+          float* __restrict__ dst, int n2, int nz2, const float* __restrict__ ecd) {
   constexpr int NT = Tr<DPN>::ND * Tr<DPN>::ND;
   __shared__ __align__(16) float sg[64][TE];
   const int t = threadIdx.x;
@@ -151,7 +205,7 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
       const int e = i % TE, g = i / TE;
       const ptrdiff_t E = E0 + e;
       float v = 0.f;
-      if (E < nelem) {
+      if (E < nelem && __ldg(ecd + E) < 0.f) {   // only non-uniform elements are stored
         const int X = (int)(E % n2), Y = (int)((E / n2) % n2), Z = (int)(E / ((ptrdiff_t)n2 * n2));
         const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
         v = __ldg(s + ((ptrdiff_t)zs(4 * Z + gz) * n0 + 4 * Y + gy) * n0 + 4 * X + gx);
@@ -176,9 +230,11 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
         }
       }
     }
+    if (tile_any) {
 #pragma unroll
-    for (int e = 0; e < TE; ++e)
-      if (E0 + e < nelem) dst[(E0 + e) * NT + t] = acc[e];
+      for (int e = 0; e < TE; ++e)
+        if (E0 + e < nelem && __ldg(ecd + E0 + e) < 0.f) dst[(E0 + e) * NT + t] = acc[e];
+    }
     __syncthreads();
   }
 }
@@ -189,19 +245,23 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
 // One CTA per coarse element, ND*ND threads (thread = matrix entry).
 template <int DPN>
 __global__ void __launch_bounds__(576)
-k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, int nzc, const WConsts Wt) {
+k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, int nzc, const WConsts Wt,
+                const float* __restrict__ ecf, const float* __restrict__ ecc, const float* __restrict__ Khf) {
   constexpr int ND = Tr<DPN>::ND;
   __shared__ float Kc[ND * ND], Tm[ND * ND];
   const int t = threadIdx.x;
   const int r = t / ND, c = t % ND;
   const int A = r / DPN, p = r % DPN, B = c / DPN, q = c % DPN;
   const int E = blockIdx.x;
+  if (__ldg(ecc + E) >= 0.f) return;            // uniform element: c Khom_l, nothing stored
   const int X = E % nc, Y = (E / nc) % nc, Z = E / (nc * nc);
   const int nfr = 2 * nc;
   float acc = 0.f;
   for (int j = 0; j < 8; ++j) {
     const int cx = 2 * X + (j & 1), cy = 2 * Y + ((j >> 1) & 1), cz = 2 * Z + (j >> 2);
-    Kc[t] = __ldg(src + (((ptrdiff_t)cz * nfr + cy) * nfr + cx) * (ND * ND) + t);
+    const ptrdiff_t child = ((ptrdiff_t)cz * nfr + cy) * nfr + cx;
+    const float cc = __ldg(ecf + child);
+    Kc[t] = cc >= 0.f ? cc * __ldg(Khf + t) : __ldg(src + child * (ND * ND) + t);
     __syncthreads();
     float tv = 0.f;   // T[(a p)][(B q)], here r = (a p)
 #pragma unroll
@@ -219,7 +279,8 @@ k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, 
 //   A_I(d) = sum_{E containing I and I+d} K_E[corner_E(I), corner_E(I+d)].
 template <int DPN>
 __global__ void __launch_bounds__(128)
-k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S, int n, int nz) {
+k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S, int n, int nz,
+                    const float* __restrict__ ecd, const float* __restrict__ ncd, const float* __restrict__ Kh) {
   constexpr int ND = Tr<DPN>::ND;
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -228,13 +289,18 @@ k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t nodes = plane * nz;
   const ptrdiff_t node = (ptrdiff_t)Z * plane + (ptrdiff_t)Y * n + X;
+  if (__ldg(ncd + node) >= 0.f) return;         // uniform / void node: nothing stored
   ptrdiff_t eidx[8];
+  float ecv[8];
   {
     const int xs0 = wrapi(X - 1, n), ys0 = wrapi(Y - 1, n), zs0 = ze(Z - 1);
 #pragma unroll
     for (int e = 0; e < 8; ++e)
+    {
       eidx[e] = (ptrdiff_t)((e >> 2) ? Z : zs0) * plane + (ptrdiff_t)(((e >> 1) & 1) ? Y : ys0) * n +
                 ((e & 1) ? X : xs0);
+      ecv[e] = __ldg(ecd + eidx[e]);
+    }
   }
 #pragma unroll
   for (int d = 0; d < 27; ++d) {
@@ -256,7 +322,8 @@ k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S
       for (int p = 0; p < DPN; ++p)
 #pragma unroll
         for (int q = 0; q < DPN; ++q)
-          A[p][q] += __ldg(Ke + eidx[e] * (ND * ND) + (kI * DPN + p) * ND + kJ * DPN + q);
+          A[p][q] += ecv[e] >= 0.f ? ecv[e] * __ldg(Kh + (kI * DPN + p) * ND + kJ * DPN + q)
+                                   : __ldg(Ke + eidx[e] * (ND * ND) + (kI * DPN + p) * ND + kJ * DPN + q);
     }
 #pragma unroll
     for (int p = 0; p < DPN; ++p)
