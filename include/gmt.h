@@ -203,6 +203,52 @@ GMT_API int gmt_op_stencil(gmt_problem p, int level, float* S);
 /* C^H of an arbitrary finest-level field u (device); CH host NRHS^2 doubles. */
 GMT_API int gmt_op_effective_tensor(gmt_problem p, const float* u, double* CH);
 
+/* ---- Slab-partitioned problems (data parallelism, Sec. 3.2 / Sec. 4.6) -------
+ * The grid is cut into P slabs of N/P z-planes.  Levels l < Ld (the
+ * "partitioned" levels, n_l/P >= 2 planes per slab, Ld >= 3 required) keep one
+ * slab per part plus one ghost plane on each side, refreshed by halo
+ * exchanges before every kernel that reads across a slab face; levels
+ * l >= Ld are small and replicated on every part (each part restricts its
+ * region into level Ld, then an all-gather completes it).  Dot products
+ * (residual norms, C^H, the zero-mean gauge) are summed over parts.  Results
+ * equal those of the single-device problem up to float rounding order.
+ * Row-level entry points and gmt_inject_correction return GMT_ERR_STATE on
+ * partitioned problems; every other entry point accepts them.
+ *
+ * Vectors/materials passed to a partitioned problem use the layout above
+ * restricted to the planes the handle holds: all N planes for
+ * gmt_create_slabs, this rank's N/P planes [z0, z0 + N/P) for gmt_create_dist
+ * (z0 = rank * N/P).  Components stay contiguous: value (m,c) of local node i
+ * is at (m*DPN + c) * (N^2 * nz_held) + i. */
+
+/* Geometry of slab `rank` of `nslabs`: info[0] = z0 (first plane), info[1] =
+ * N/P planes, info[2] = Ld (number of partitioned levels; L when nslabs==1),
+ * info[3] = L.  Host only.  GMT_ERR_ARG if the partition is not possible. */
+GMT_API int gmt_slab_layout(int res, int levels, int nslabs, int rank, int* info);
+
+/* P slabs on one device (cfg->device), exchanging ghost planes by device
+ * copies on one stream: the partitioned algorithm without a second GPU.
+ * material: the full N^3 field.  The returned handle owns all slabs. */
+GMT_API int gmt_create_slabs(const gmt_config* cfg, const void* material, int material_dtype,
+                             int material_location, int nslabs, gmt_problem* out);
+
+/* NCCL unique id for gmt_create_dist (call on one rank, broadcast the bytes).
+ * id: host buffer of len >= 128 bytes.  GMT_ERR_NCCL if libnccl.so.2 cannot
+ * be loaded (NCCL is dlopen'ed at first use). */
+GMT_API int gmt_nccl_unique_id(void* id, size_t len);
+
+/* Slab `rank` of an `nranks`-process job, one process per GPU (cfg->device).
+ * Halo planes travel by ncclSend/ncclRecv, the replicated level by
+ * ncclAllGather, dot products by ncclAllReduce, all on the problem stream.
+ * Collective: every rank must call it (and every later entry point) in the
+ * same order.  material_slab: this rank's N/P planes. */
+GMT_API int gmt_create_dist(const gmt_config* cfg, const void* material_slab, int material_dtype,
+                            int material_location, int rank, int nranks, const void* nccl_id,
+                            gmt_problem* out);
+
+/* Number of slabs of the problem (1 for gmt_create). */
+GMT_API int gmt_num_slabs(gmt_problem p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,6 +2,8 @@
 // declared in include/gmt.h.  One translation unit: the kernel headers are
 // included here so every template is instantiated next to its launcher.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -12,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -54,7 +57,11 @@ int fail(int code, const char* fmt, ...) {
 
 struct LevelBuf {
   int n = 0, nz = 0;
-  size_t nodes = 0;
+  size_t nodes = 0;        // local nodes (n * n * nz)
+  ptrdiff_t cs = 0;        // component stride of vectors (nodes + ghost planes)
+  int gh = 0;              // ghost planes per side of vectors (slab-partitioned levels)
+  int zoff = 0;            // first global plane of this slab at this level
+  bool dist = false;       // level is slab-partitioned (ghost planes), else replicated / single GPU
   float* u = nullptr;    // solution / coarse error
   float* t = nullptr;    // Jacobi ping-pong partner
   float* f = nullptr;    // right-hand side (levels >= 1)
@@ -88,6 +95,8 @@ Geo geo(int n, int nz) {
   g.nblk = g.grid.x * g.grid.y * g.grid.z;
   return g;
 }
+
+struct Group;   // slab partition (gmt_group.inc)
 
 }  // namespace
 
@@ -140,8 +149,18 @@ struct gmt_problem_s {
   double prof_ms[8] = {0};
   long long prof_cnt[8] = {0};
 
-  ZMap zm(int l) const { return ZMap{lv[l].nz, 1}; }
+  // slab partition (multi-GPU / virtual slabs): levels < Ld are z-slabs with
+  // one ghost plane per side, levels >= Ld are replicated on every slab
+  Group* grp = nullptr;
+  int P = 1, rank = 0, Ld = 0;
+
+  ZMap zm(int l) const { return lv[l].dist ? ZMap{lv[l].nz, 0, 0} : ZMap{lv[l].nz, 1, 0}; }
 };
+
+// Ghost planes of the level-0 per-voxel / per-node arrays (allocated in every
+// mode; used when slab-partitioned).
+constexpr int MAT_GLO = 2, MAT_GHI = 1;   // material: voxel planes -2..-1, nz
+constexpr int TF_GLO = 3, TF_GHI = 2;     // tile flags: planes -3..-1, nz..nz+1 (set to 1 = active)
 
 namespace {
 
@@ -156,12 +175,30 @@ int dalloc(gmt_problem p, void** ptr, size_t bytes) {
   return GMT_OK;
 }
 
+// Vector storage: component planes with `gh` ghost planes on each side of a
+// slab-partitioned level; the vector pointer addresses plane 0 of component 0.
+inline float* vbase(const LevelBuf& b, float* v) { return v - (ptrdiff_t)b.gh * b.n * b.n; }
+inline size_t vbytes(gmt_problem p, const LevelBuf& b) { return (size_t)p->V * b.cs * sizeof(float); }
+
+// user layout [m][c][z][y][x] (component stride = nodes)  <->  internal layout
+int copy_in(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cudaMemcpyKind kind) {
+  const size_t w = b.nodes * sizeof(float);
+  CK(cudaMemcpy2DAsync(dst, b.cs * sizeof(float), src, w, w, p->V, kind, p->stream));
+  return GMT_OK;
+}
+int copy_out(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cudaMemcpyKind kind) {
+  const size_t w = b.nodes * sizeof(float);
+  CK(cudaMemcpy2DAsync(dst, w, src, b.cs * sizeof(float), w, p->V, kind, p->stream));
+  return GMT_OK;
+}
+
 int set_device(gmt_problem p) {
   CK(cudaSetDevice(p->cfg.device));
   return GMT_OK;
 }
 
 void drop_graph(gmt_problem p);
+void drop_group_graph(Group* G);
 
 // ---------------------------------------------------------------- accounting
 
@@ -219,7 +256,7 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   cudaStream_t st = p->stream;
   const float om = (float)p->cfg.omega;
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
-  const ptrdiff_t cs = (ptrdiff_t)b.nodes;
+  const ptrdiff_t cs = b.cs;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
     const bool packed = DPN == 3 && p->variant == 1;
     const int NRG = DPN == 3 ? (packed ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
@@ -304,7 +341,7 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
   const float* sd = skip_void ? bc.ncode : nullptr;
   const float* actf = l == 0 ? p->code : bf.ncode;
   k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
-                                                      (ptrdiff_t)bf.nodes, (ptrdiff_t)bc.nodes, actf);
+                                                      bf.cs, bc.cs, actf);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -316,12 +353,10 @@ int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
   Prof prof(p, l == 0 ? 2 : 4);
   if (l == 0)
     k_prolong_add<DPN, true><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
-                                                                 p->s, p->zm(0), nullptr, (ptrdiff_t)bf.nodes,
-                                                                 (ptrdiff_t)bc.nodes);
+                                                                 p->s, p->zm(0), nullptr, bf.cs, bc.cs);
   else
     k_prolong_add<DPN, false><<<g.grid, g.block, 0, p->stream>>>(
-        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0), bf.ncode, (ptrdiff_t)bf.nodes,
-        (ptrdiff_t)bc.nodes);
+        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0), bf.ncode, bf.cs, bc.cs);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -336,7 +371,7 @@ int smooth(gmt_problem p, int l, int sweeps) {
     TRY(launch_op<DPN>(p, l, M_JACOBI, src, f, dst, nullptr, 1));
   }
   if (sweeps & 1)
-    CK(cudaMemcpyAsync(b.u, b.t, b.nodes * p->V * sizeof(float), cudaMemcpyDeviceToDevice, p->stream));
+    CK(cudaMemcpyAsync(vbase(b, b.u), vbase(b, b.t), vbytes(p, b), cudaMemcpyDeviceToDevice, p->stream));
   return GMT_OK;
 }
 
@@ -362,9 +397,8 @@ int vcycle_once(gmt_problem p) {
     TRY(smooth<DPN>(p, l, p->cfg.pre_sweeps));                                  // pre-smoothing
     TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? nullptr : b.f, b.r, nullptr, 1));  // r = f - K u
     TRY(launch_restrict<DPN>(p, l, b.r, c.f, true));                             // f^{l+1} = R r^l
-    const size_t vb = c.nodes * p->V * sizeof(float);
-    if (c.inj_pending) CK(cudaMemcpyAsync(c.u, c.inj, vb, cudaMemcpyDeviceToDevice, p->stream));
-    else CK(cudaMemsetAsync(c.u, 0, vb, p->stream));                             // u^{l+1} = 0 / e_hat
+    if (c.inj_pending) TRY(copy_in(p, c, c.u, c.inj, cudaMemcpyDeviceToDevice));
+    else CK(cudaMemsetAsync(vbase(c, c.u), 0, vbytes(p, c), p->stream));        // u^{l+1} = 0 / e_hat
   }
   TRY(coarsest<DPN>(p));                                                         // coarsest solve
   for (int l = L - 2; l >= 0; --l) {
@@ -392,7 +426,8 @@ int build_operators(gmt_problem p) {
   {
     // static interface-node list (sorted, deterministic)
     const size_t total = p->lv[0].nodes;
-    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag, p->code);
+    const int zlo = p->lv[0].dist ? -1 : 0, zhi = p->lv[0].nz + (p->lv[0].dist ? 1 : 0);
+    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag, p->code, zlo, zhi);
     LAUNCHED(p);
     cub::CountingInputIterator<int> it(0);
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
@@ -464,8 +499,9 @@ int build_operators(gmt_problem p) {
   return GMT_OK;
 }
 
-int upload_material(gmt_problem p, const void* material, int dtype, int location) {
-  const size_t nvox = (size_t)p->N * p->N * p->N;
+// Write `count` voxels (default: the whole local grid) into p->s[0, count).
+int upload_material(gmt_problem p, const void* material, int dtype, int location, size_t count = 0) {
+  const size_t nvox = count ? count : p->lv[0].nodes;
   if (!material) return fail(GMT_ERR_ARG, "material is NULL");
   if (dtype == GMT_F32) {
     CK(cudaMemcpyAsync(p->s, material, nvox * sizeof(float),
@@ -492,7 +528,7 @@ int upload_material(gmt_problem p, const void* material, int dtype, int location
 // beyond resetting the solution.
 int reset_solution(gmt_problem p) {
   for (auto& b : p->lv) {
-    CK(cudaMemsetAsync(b.u, 0, b.nodes * p->V * sizeof(float), p->stream));
+    CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
     b.inj_pending = false;
   }
   return GMT_OK;
@@ -528,7 +564,7 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
   {
     Prof prof(p, 7);
     k_effective_tensor<DPN><<<nblk, 128, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
-                                                         (float)p->ed.mu, p->part, (ptrdiff_t)b.nodes, p->elist,
+                                                         (float)p->ed.mu, p->part, b.cs, p->elist,
                                                          p->ecount);
     LAUNCHED(p);
   }
@@ -580,6 +616,7 @@ int zero_mean(gmt_problem p, float* dst) {
 }
 
 void drop_graph(gmt_problem p) {
+  if (p->grp) drop_group_graph(p->grp);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   p->gexec = nullptr;
   p->graph_ok = false;
@@ -593,18 +630,32 @@ void free_all(gmt_problem p) {
   for (cudaEvent_t e : p->pool) cudaEventDestroy(e);
   p->pool.clear();
   for (auto& b : p->lv) {
-    cudaFree(b.u); cudaFree(b.t); cudaFree(b.f); cudaFree(b.r);
-    cudaFree(b.S); cudaFree(b.Ke); cudaFree(b.inj);
-    cudaFree(b.ecode); cudaFree(b.ncode); cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.tflag); cudaFree(b.ilist);
+    for (float* v : {b.u, b.t, b.f, b.r})
+      if (v) cudaFree(vbase(b, v));
+    const size_t pl = (size_t)b.n * b.n;
+    cudaFree(b.S); cudaFree(b.inj);
+    if (b.Ke) cudaFree(b.Ke - pl * 576 / (p->dpn == 3 ? 1 : 9));
+    if (b.ecode) cudaFree(b.ecode - pl);
+    if (b.ncode) cudaFree(b.ncode - pl);
+    if (b.tflag) cudaFree(b.tflag - (size_t)b.tntx * b.tnty * TF_GLO);
+    cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.ilist);
   }
-  cudaFree(p->s); cudaFree(p->M1g); cudaFree(p->M2g); cudaFree(p->tflag);
-  cudaFree(p->iflag); cudaFree(p->code); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  if (p->s) cudaFree(p->s - (size_t)p->N * p->N * MAT_GLO);
+  cudaFree(p->M1g); cudaFree(p->M2g);
+  if (p->tflag) cudaFree(p->tflag - (size_t)p->tntx * p->tnty * TF_GLO);
+  cudaFree(p->iflag);
+  if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
 }
 
+int no_group(gmt_problem p) {
+  return p->grp ? fail(GMT_ERR_STATE, "not available on slab-partitioned problems") : GMT_OK;
+}
+
 int check_level(gmt_problem p, int level, bool allow_coarsest = true) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (p->grp) return fail(GMT_ERR_STATE, "row-level entry points act on single-device problems only");
   if (level < 0 || level >= p->L || (!allow_coarsest && level >= p->L - 1))
     return fail(GMT_ERR_ARG, "level %d out of range (L=%d)", level, p->L);
   return GMT_OK;
@@ -641,8 +692,24 @@ int gmt_default_config(gmt_config* cfg, int physics, int res) {
   return GMT_OK;
 }
 
-int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtype, int material_location,
-               gmt_problem* out) {
+}  // extern "C"
+
+namespace {
+
+// Slab geometry: level-0 slab of nz0 = N/P planes at z0 = rank*nz0; levels
+// l < Ld are partitioned (nz0 >> l >= 2 planes), levels >= Ld replicated.
+int slab_levels(int N, int L, int P, int* Ld_out) {
+  if (P == 1) { *Ld_out = 0; return GMT_OK; }
+  if (N % P) return fail(GMT_ERR_ARG, "res %d not divisible by %d slabs", N, P);
+  const int nz0 = N / P;
+  int Ld = 0;
+  while (Ld < L - 1 && nz0 % (1 << Ld) == 0 && (nz0 >> Ld) >= 2) ++Ld;
+  if (Ld < 3) return fail(GMT_ERR_ARG, "slab partition needs >= 3 partitioned levels (res %d, %d slabs)", N, P);
+  *Ld_out = Ld;
+  return GMT_OK;
+}
+
+int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_stream, gmt_problem* out) {
   if (!cfg_in || !out) return fail(GMT_ERR_ARG, "null argument");
   *out = nullptr;
   gmt_config cfg = *cfg_in;
@@ -662,8 +729,13 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   if (cfg.res % (1 << (L - 1)) != 0) return fail(GMT_ERR_ARG, "res %d not divisible by 2^(L-1)", cfg.res);
   if ((cfg.res >> (L - 1)) < 2) return fail(GMT_ERR_ARG, "coarsest resolution must be >= 2");
   cfg.levels = L;
+  int Ld = 0;
+  TRY(slab_levels(cfg.res, L, P, &Ld));
 
   gmt_problem p = new gmt_problem_s();
+  p->P = P;
+  p->rank = rank;
+  p->Ld = Ld;
   p->cfg = cfg;
   p->N = cfg.res;
   p->L = L;
@@ -692,7 +764,9 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
     return code;
   };
   if ((rc = set_device(p)) != GMT_OK) return bail(rc);
-  if (cfg.stream) {
+  if (shared_stream) {
+    p->stream = shared_stream;
+  } else if (cfg.stream) {
     p->stream = (cudaStream_t)cfg.stream;
   } else {
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -708,38 +782,70 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   for (int l = 0; l < L; ++l) {
     LevelBuf& b = p->lv[l];
     b.n = cfg.res >> l;
-    b.nz = b.n;
+    b.dist = l < Ld;
+    b.nz = b.dist ? (cfg.res / P) >> l : b.n;
+    b.gh = b.dist ? 1 : 0;
+    b.zoff = ((cfg.res / P) * rank) >> l;   // slab origin at this level (first replicated level: region)
     b.nodes = (size_t)b.n * b.n * b.nz;
-    const size_t vb = b.nodes * V * sizeof(float);
-    if ((rc = dalloc(p, (void**)&b.u, vb)) || (rc = dalloc(p, (void**)&b.t, vb))) return bail(rc);
-    if (l >= 1 && (rc = dalloc(p, (void**)&b.f, vb))) return bail(rc);
-    if ((l < L - 1 || l == 0) && (rc = dalloc(p, (void**)&b.r, vb))) return bail(rc);
+    b.cs = (ptrdiff_t)b.n * b.n * (b.nz + 2 * b.gh);
+    const size_t vb = (size_t)V * b.cs * sizeof(float);
+    const ptrdiff_t goff = (ptrdiff_t)b.gh * b.n * b.n;
+    auto valloc = [&](float** v) -> int {
+      const int r = dalloc(p, (void**)v, vb);
+      if (r == GMT_OK) *v += goff;
+      return r;
+    };
+    if ((rc = valloc(&b.u)) || (rc = valloc(&b.t))) return bail(rc);
+    if (l >= 1 && (rc = valloc(&b.f))) return bail(rc);
+    if ((l < L - 1 || l == 0) && (rc = valloc(&b.r))) return bail(rc);
     if (l >= 1 && (rc = dalloc(p, (void**)&b.S, b.nodes * 27 * p->dpn * p->dpn * sizeof(float)))) return bail(rc);
-    if (l >= 2 && (rc = dalloc(p, (void**)&b.Ke, b.nodes * nd * nd * sizeof(float)))) return bail(rc);
-    if (l >= 1 && ((rc = dalloc(p, (void**)&b.ecode, b.nodes * sizeof(float))) ||
-                   (rc = dalloc(p, (void**)&b.ncode, b.nodes * sizeof(float)))))
-      return bail(rc);
+    const size_t pl = (size_t)b.n * b.n;   // one plane
+    // element / node codes and element matrices carry one ghost plane below
+    if (l >= 2) {
+      if ((rc = dalloc(p, (void**)&b.Ke, (b.nodes + pl) * nd * nd * sizeof(float)))) return bail(rc);
+      b.Ke += pl * nd * nd;
+    }
+    if (l >= 1) {
+      if ((rc = dalloc(p, (void**)&b.ecode, (b.nodes + pl) * sizeof(float))) ||
+          (rc = dalloc(p, (void**)&b.ncode, (b.nodes + pl) * sizeof(float))))
+        return bail(rc);
+      b.ecode += pl;
+      b.ncode += pl;
+    }
     if ((rc = dalloc(p, (void**)&b.Hl, 27 * 9 * sizeof(float))) || (rc = dalloc(p, (void**)&b.Kh, 576 * sizeof(float))))
       return bail(rc);
     b.tiled = l >= 1 && l < L - 1 && b.n >= coarse_tiled_min;
     if (b.tiled) {
       b.tntx = (b.n + TT_X - 1) / TT_X;
       b.tnty = (b.n + TT_Y - 1) / TT_Y;
-      if ((rc = dalloc(p, (void**)&b.tflag, (size_t)b.tntx * b.tnty * b.nz)) ||
+      const size_t tfp = (size_t)b.tntx * b.tnty;
+      if ((rc = dalloc(p, (void**)&b.tflag, tfp * (b.nz + TF_GLO + TF_GHI))) ||
           (rc = dalloc(p, (void**)&b.ilist, b.nodes * sizeof(int))))
         return bail(rc);
+      if (cudaMemset(b.tflag, 1, tfp * (b.nz + TF_GLO + TF_GHI)) != cudaSuccess)
+        return bail(fail(GMT_ERR_CUDA, "memset failed"));
+      b.tflag += tfp * TF_GLO;
     }
     max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
   }
   p->part_cap = (2 * max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
   if ((rc = dalloc(p, (void**)&p->part, p->part_cap * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->red, 64 * sizeof(double)))) return bail(rc);
-  if ((rc = dalloc(p, (void**)&p->s, (size_t)p->N * p->N * p->N * sizeof(float)))) return bail(rc);
+  const size_t pl0 = (size_t)p->N * p->N;
+  if ((rc = dalloc(p, (void**)&p->s, pl0 * (p->lv[0].nz + MAT_GLO + MAT_GHI) * sizeof(float)))) return bail(rc);
+  p->s += pl0 * MAT_GLO;
   p->tntx = (cfg.res + TT_X - 1) / TT_X;
   p->tnty = (cfg.res + TT_Y - 1) / TT_Y;
-  if ((rc = dalloc(p, (void**)&p->tflag, (size_t)p->tntx * p->tnty * p->lv[0].nz))) return bail(rc);
+  {
+    const size_t tfp = (size_t)p->tntx * p->tnty;
+    if ((rc = dalloc(p, (void**)&p->tflag, tfp * (p->lv[0].nz + TF_GLO + TF_GHI)))) return bail(rc);
+    if (cudaMemset(p->tflag, 1, tfp * (p->lv[0].nz + TF_GLO + TF_GHI)) != cudaSuccess)
+      return bail(fail(GMT_ERR_CUDA, "memset failed"));
+    p->tflag += tfp * TF_GLO;
+  }
   if ((rc = dalloc(p, (void**)&p->iflag, p->lv[0].nodes))) return bail(rc);
-  if ((rc = dalloc(p, (void**)&p->code, p->lv[0].nodes * sizeof(float)))) return bail(rc);
+  if ((rc = dalloc(p, (void**)&p->code, (p->lv[0].nodes + 2 * pl0) * sizeof(float)))) return bail(rc);
+  p->code += pl0;   // node codes of planes -1 .. nz
   if ((rc = dalloc(p, (void**)&p->ilist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->elist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->eflag, p->lv[0].nodes))) return bail(rc);
@@ -801,15 +907,37 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
   // zero every vector once: values at inactive nodes are never read except as
   // (zero-coefficient) neighbours, so they must be finite
   for (auto& b : p->lv) {
-    const size_t vb = b.nodes * p->V * sizeof(float);
     for (float* v : {b.u, b.t, b.f, b.r})
-      if (v && cudaMemsetAsync(v, 0, vb, p->stream) != cudaSuccess) return bail(fail(GMT_ERR_CUDA, "memset failed"));
+      if (v && cudaMemsetAsync(vbase(b, v), 0, vbytes(p, b), p->stream) != cudaSuccess)
+        return bail(fail(GMT_ERR_CUDA, "memset failed"));
   }
-  if ((rc = upload_material(p, material, material_dtype, material_location))) return bail(rc);
-  if ((rc = rebuild(p))) return bail(rc);
   if (cudaStreamSynchronize(p->stream) != cudaSuccess) {
     cudaError_t e = cudaGetLastError();
-    return bail(fail(GMT_ERR_CUDA, "setup failed: %s", cudaGetErrorString(e)));
+    return bail(fail(GMT_ERR_CUDA, "allocation failed: %s", cudaGetErrorString(e)));
+  }
+  *out = p;
+  return GMT_OK;
+}
+
+#include "gmt_group.inc"
+void drop_group_graph(Group* G) { g_drop_graph(G); }
+
+}  // namespace
+
+extern "C" {
+
+int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtype, int material_location,
+               gmt_problem* out) {
+  gmt_problem p = nullptr;
+  TRY(create_impl(cfg_in, 1, 0, nullptr, &p));
+  int rc;
+  if ((rc = upload_material(p, material, material_dtype, material_location)) || (rc = rebuild(p)) ||
+      (rc = (cudaStreamSynchronize(p->stream) == cudaSuccess ? GMT_OK
+                                                              : fail(GMT_ERR_CUDA, "setup failed: %s",
+                                                                     cudaGetErrorString(cudaGetLastError()))))) {
+    free_all(p);
+    delete p;
+    return rc;
   }
   *out = p;
   return GMT_OK;
@@ -818,6 +946,7 @@ int gmt_create(const gmt_config* cfg_in, const void* material, int material_dtyp
 int gmt_set_material(gmt_problem p, const void* material, int dtype, int location) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
+  if (p->grp) return g_set_material(p->grp, material, dtype, location);
   TRY(upload_material(p, material, dtype, location));
   TRY(rebuild(p));
   return GMT_OK;
@@ -826,18 +955,17 @@ int gmt_set_material(gmt_problem p, const void* material, int dtype, int locatio
 int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
+  if (p->grp) return g_set_initial_guess(p->grp, u, location);
   LevelBuf& b = p->lv[0];
-  const size_t vb = b.nodes * p->V * sizeof(float);
-  if (!u) CK(cudaMemsetAsync(b.u, 0, vb, p->stream));
-  else
-    CK(cudaMemcpyAsync(b.u, u, vb, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                       p->stream));
+  if (!u) CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
+  else TRY(copy_in(p, b, b.u, u, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
   return GMT_OK;
 }
 
 int gmt_inject_correction(gmt_problem p, int level, const float* e, int location) {
   TRY(check_level(p, level));
   if (level < 1) return fail(GMT_ERR_ARG, "injection level must be >= 1");
+  TRY(no_group(p));
   TRY(set_device(p));
   LevelBuf& b = p->lv[level];
   if (!e) { b.inj_pending = false; return GMT_OK; }
@@ -853,6 +981,7 @@ int gmt_vcycle(gmt_problem p, int ncycles) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   if (ncycles < 0) return fail(GMT_ERR_ARG, "ncycles < 0");
   TRY(set_device(p));
+  if (p->grp) return g_vcycle(p->grp, ncycles);
   for (int c = 0; c < ncycles; ++c) {
     bool inj = false;
     for (auto& b : p->lv) inj |= b.inj_pending;
@@ -921,11 +1050,19 @@ int gmt_profile_read(gmt_problem p, int cls, double* total_ms, long long* launch
   return GMT_OK;
 }
 
-long long gmt_kernel_launches(gmt_problem p) { return p ? p->launches : 0; }
+long long gmt_kernel_launches(gmt_problem p) {
+  if (!p) return 0;
+  if (!p->grp) return p->launches;
+  long long n = 0;
+  for (auto q : p->grp->slabs) n += q->launches;
+  return n;
+}
 
 int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
+  if (p->grp)
+    return p->dpn == 3 ? g_residual_norms<3>(p->grp, rel, abs_r, abs_f) : g_residual_norms<1>(p->grp, rel, abs_r, abs_f);
   return p->dpn == 3 ? residual_norms<3>(p, rel, abs_r, abs_f) : residual_norms<1>(p, rel, abs_r, abs_f);
 }
 
@@ -954,21 +1091,24 @@ int gmt_solve(gmt_problem p, double rel_tol, int max_cycles, int* cycles_done, d
 int gmt_homogenize(gmt_problem p, double* CH) {
   if (!p || !CH) return fail(GMT_ERR_ARG, "null argument");
   TRY(set_device(p));
+  if (p->grp) return p->dpn == 3 ? g_effective_tensor<3>(p->grp, CH) : g_effective_tensor<1>(p->grp, CH);
   return p->dpn == 3 ? effective_tensor<3>(p, p->lv[0].u, CH) : effective_tensor<1>(p, p->lv[0].u, CH);
 }
 
 int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) {
   if (!p || !u) return fail(GMT_ERR_ARG, "null argument");
   TRY(set_device(p));
+  if (p->grp) return g_get_solution(p->grp, u, location, zero_mean_flag);
   LevelBuf& b = p->lv[0];
-  const size_t vb = b.nodes * p->V * sizeof(float);
-  float* dst = (location == GMT_DEVICE) ? u : b.t;   // t is scratch between cycles
-  CK(cudaMemcpyAsync(dst, b.u, vb, cudaMemcpyDeviceToDevice, p->stream));
+  // user-layout working copy: the caller's device buffer, or the residual
+  // buffer's storage (scratch between cycles, large enough for nodes * V)
+  float* dst = (location == GMT_DEVICE) ? u : vbase(b, b.r);
+  TRY(copy_out(p, b, dst, b.u, cudaMemcpyDeviceToDevice));
   k_mask_inactive<<<1184, 256, 0, p->stream>>>(p->code, dst, b.nodes, p->V);   // inactive nodes -> 0
   LAUNCHED(p);
   if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
   if (location == GMT_HOST) {
-    CK(cudaMemcpyAsync(u, dst, vb, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaMemcpyAsync(u, dst, b.nodes * p->V * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
     CK(cudaStreamSynchronize(p->stream));
   }
   return GMT_OK;
@@ -976,7 +1116,7 @@ int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) 
 
 int gmt_num_levels(gmt_problem p) { return p ? p->L : GMT_ERR_ARG; }
 int gmt_level_res(gmt_problem p, int level) {
-  if (check_level(p, level) != GMT_OK) return GMT_ERR_ARG;
+  if (!p || level < 0 || level >= p->L) return fail(GMT_ERR_ARG, "level %d out of range", level);
   return p->lv[level].n;
 }
 int gmt_nrhs(gmt_problem p) { return p ? p->nr : GMT_ERR_ARG; }
@@ -994,6 +1134,10 @@ int gmt_sync(gmt_problem p) {
 void gmt_destroy(gmt_problem p) {
   if (!p) return;
   cudaSetDevice(p->cfg.device);
+  if (p->grp) {
+    if (p == p->grp->slabs[0]) g_destroy(p->grp);   // other slab handles are owned by the group
+    return;
+  }
   if (p->stream) cudaStreamSynchronize(p->stream);
   free_all(p);
   delete p;
@@ -1042,6 +1186,7 @@ int gmt_op_prolong_add(gmt_problem p, int level, const float* e, float* u) {
 
 int gmt_op_loads(gmt_problem p, float* f) {
   if (!p || !f) return fail(GMT_ERR_ARG, "null argument");
+  TRY(no_group(p));
   TRY(set_device(p));
   return p->dpn == 3 ? launch_op<3>(p, 0, M_LOADS, p->lv[0].u, nullptr, f, nullptr)
                      : launch_op<1>(p, 0, M_LOADS, p->lv[0].u, nullptr, f, nullptr);
@@ -1068,8 +1213,53 @@ int gmt_op_stencil(gmt_problem p, int level, float* S) {
 
 int gmt_op_effective_tensor(gmt_problem p, const float* u, double* CH) {
   if (!p || !u || !CH) return fail(GMT_ERR_ARG, "null argument");
+  TRY(no_group(p));
   TRY(set_device(p));
   return p->dpn == 3 ? effective_tensor<3>(p, u, CH) : effective_tensor<1>(p, u, CH);
 }
+
+// ---- slab-partitioned problems (gmt_group.inc)
+
+int gmt_slab_layout(int res, int levels, int nslabs, int rank, int* info) {
+  if (!info || res < 2 || nslabs < 1 || rank < 0 || rank >= nslabs) return fail(GMT_ERR_ARG, "bad argument");
+  int L = levels;
+  if (L <= 0) {
+    L = 1;
+    int m = res;
+    while (m % 2 == 0 && m / 2 >= 4) { m /= 2; ++L; }
+  }
+  if (res % (1 << (L - 1)) != 0) return fail(GMT_ERR_ARG, "res %d not divisible by 2^(L-1)", res);
+  int Ld = 0;
+  TRY(slab_levels(res, L, nslabs, &Ld));
+  const int nz0 = res / nslabs;
+  info[0] = nz0 * rank;
+  info[1] = nz0;
+  info[2] = nslabs == 1 ? L : Ld;
+  info[3] = L;
+  return GMT_OK;
+}
+
+int gmt_create_slabs(const gmt_config* cfg, const void* material, int material_dtype, int material_location,
+                     int nslabs, gmt_problem* out) {
+  return g_create(cfg, material, material_dtype, material_location, nslabs, 0, nullptr, out);
+}
+
+int gmt_nccl_unique_id(void* id, size_t len) {
+  if (!id || len < sizeof(ncclUniqueId)) return fail(GMT_ERR_ARG, "id buffer must hold %zu bytes", sizeof(ncclUniqueId));
+  NcclApi* A = nccl_api();
+  if (!A) return fail(GMT_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId u;
+  NK(A->getUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return GMT_OK;
+}
+
+int gmt_create_dist(const gmt_config* cfg, const void* material_slab, int material_dtype, int material_location,
+                    int rank, int nranks, const void* nccl_id, gmt_problem* out) {
+  if (!nccl_id) return fail(GMT_ERR_ARG, "nccl_id is NULL");
+  return g_create(cfg, material_slab, material_dtype, material_location, nranks, rank, nccl_id, out);
+}
+
+int gmt_num_slabs(gmt_problem p) { return !p ? GMT_ERR_ARG : (p->grp ? p->grp->P : 1); }
 
 }  // extern "C"

@@ -18,10 +18,14 @@ template <int DPN> struct Tr {
 // (multi-GPU): planes -g..-1 and nz..nz+g-1 are ghost planes that live in
 // the same allocation, so indices are used as-is.
 struct ZMap {
-  int nz;
-  int wrap;
+  int nz;        // periodic extent when wrapping (the global plane count of a replicated level)
+  int wrap;      // 1: periodic wrap; 0: slab with ghost planes (index used as is)
+  int off = 0;   // wrap mode: plane offset of this slab inside a replicated level
   __device__ __forceinline__ int operator()(int p) const {
-    if (wrap) { if (p < 0) p += nz; else if (p >= nz) p -= nz; }
+    if (wrap) {
+      p += off;
+      if (p < 0) p += nz; else if (p >= nz) p -= nz;
+    }
     return p;
   }
 };

@@ -314,12 +314,15 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
 
 // Interface nodes: those whose 8 incident voxels are not all equal (the
 // material interface).  flag = 1 per interface node (level 0).
+// Node codes are produced for planes [zlo, zhi) (ghost planes included when
+// slab-partitioned), interface flags for the local planes [0, nz).
 __global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int nz, uint8_t* __restrict__ flag,
-                              float* __restrict__ code) {
+                              float* __restrict__ code, int zlo, int zhi) {
   const ptrdiff_t plane = (ptrdiff_t)n * n;
-  const ptrdiff_t total = plane * nz;
-  for (ptrdiff_t i = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; i < total; i += (ptrdiff_t)gridDim.x * blockDim.x) {
-    const int x = (int)(i % n), y = (int)((i / n) % n), z = (int)(i / plane);
+  const ptrdiff_t total = plane * (zhi - zlo);
+  for (ptrdiff_t ii = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; ii < total; ii += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const ptrdiff_t i = ii + (ptrdiff_t)zlo * plane;
+    const int x = (int)(ii % n), y = (int)((ii / n) % n), z = (int)(ii / plane) + zlo;
     const int xm = wrapi(x - 1, n), ym = wrapi(y - 1, n), zm = zs(z - 1);
     const float s0 = __ldg(s + (ptrdiff_t)zm * plane + (ptrdiff_t)ym * n + xm);
     bool uni = true;
@@ -328,7 +331,7 @@ __global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int n
       const ptrdiff_t idx = ((e >> 2) ? z : zm) * plane + (ptrdiff_t)(((e >> 1) & 1) ? y : ym) * n + ((e & 1) ? x : xm);
       uni &= (__ldg(s + idx) == s0);
     }
-    flag[i] = uni ? 0 : 1;
+    if (z >= 0 && z < nz) flag[i] = uni ? 0 : 1;
     code[i] = uni ? s0 : -1.f;
   }
 }

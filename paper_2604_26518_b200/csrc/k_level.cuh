@@ -363,9 +363,9 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
     act = __ldg(Sdiag + node) != 0.f;
   }
   if (!act) return;
-  const int X0 = x >> 1, Y0 = y >> 1, Z0 = z >> 1;
+  const int X0 = x >> 1, Y0 = y >> 1, Zl = z >> 1;
   const int rx = x & 1, ry = y & 1, rz = z & 1;
-  const int X1 = wrapi(X0 + 1, nc), Y1 = wrapi(Y0 + 1, nc), Z1 = zc(Z0 + 1);
+  const int X1 = wrapi(X0 + 1, nc), Y1 = wrapi(Y0 + 1, nc), Z0 = zc(Zl), Z1 = zc(Zl + 1);
   const ptrdiff_t pc = (ptrdiff_t)nc * nc;
   float acc[V];
   load_node<DPN>(u + node, csf, acc);

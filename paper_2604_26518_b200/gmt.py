@@ -74,6 +74,13 @@ SIGNATURES = {
     "gmt_op_diagonal": (C.c_int, [_P, C.c_int, _FP]),
     "gmt_op_stencil": (C.c_int, [_P, C.c_int, _FP]),
     "gmt_op_effective_tensor": (C.c_int, [_P, _FP, _DP]),
+    "gmt_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "gmt_create_slabs": (C.c_int, [C.POINTER(gmt_config), C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_void_p)]),
+    "gmt_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "gmt_create_dist": (C.c_int, [C.POINTER(gmt_config), C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_void_p, C.POINTER(C.c_void_p)]),
+    "gmt_num_slabs": (C.c_int, [_P]),
 }
 
 _lib = None
@@ -134,17 +141,37 @@ def _dptr(a):
     return p
 
 
+def gmt_slab_layout(res: int, levels: int, nslabs: int, rank: int) -> dict:
+    """Slab geometry (host only): z0, nz, Ld (partitioned levels), L."""
+    lib = load()
+    info = (C.c_int * 4)()
+    _check(lib.gmt_slab_layout(res, levels, nslabs, rank, info), "gmt_slab_layout")
+    return {"z0": info[0], "nz": info[1], "Ld": info[2], "L": info[3]}
+
+
+def gmt_nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for gmt_create_dist (create on rank 0, broadcast)."""
+    lib = load()
+    buf = C.create_string_buffer(128)
+    _check(lib.gmt_nccl_unique_id(buf, 128), "gmt_nccl_unique_id")
+    return buf.raw
+
+
 class Problem:
-    """One periodic cell problem set (all load cases) on one GPU: gmt_create."""
+    """One periodic cell problem set (all load cases): gmt_create on one GPU,
+    gmt_create_slabs (slabs=P: P z-slabs on one GPU with device-copy halos), or
+    gmt_create_dist (dist=(rank, nranks, nccl_id): this rank's slab of an
+    NCCL job; `material` then holds this rank's N/P planes)."""
 
     def __init__(self, material, physics: str = "elastic", levels: int = 0, E: float = 1.0,
                  nu: float = 0.3, kappa: float = 1.0, omega: float = 0.0, pre_sweeps: int = 2,
                  post_sweeps: int = 2, coarse_sweeps: int = 16, device: int = 0, stream=None,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, slabs: int = 1, dist=None):
         lib = load()
-        n = int(material.shape[0])
-        if tuple(material.shape) != (n, n, n):
-            raise ValueError("material must be (N, N, N)")
+        n = int(material.shape[1])
+        nz = int(material.shape[0])
+        if tuple(material.shape[1:]) != (n, n) or (dist is None and nz != n):
+            raise ValueError("material must be (N, N, N) (or (N/P, N, N) for dist)")
         cfg = gmt_config()
         _check(lib.gmt_default_config(C.byref(cfg), PHYSICS[physics], n), "gmt_default_config")
         cfg.levels, cfg.E, cfg.nu, cfg.kappa, cfg.omega = levels, E, nu, kappa, omega
@@ -154,8 +181,19 @@ class Problem:
         cfg.use_graphs = int(use_graphs)
         ptr, loc, dt = self._material(material)
         h = C.c_void_p()
-        _check(lib.gmt_create(C.byref(cfg), ptr, dt, loc, C.byref(h)), "gmt_create")
+        if dist is not None:
+            rank, nranks, nid = dist
+            if nz * nranks != n:
+                raise ValueError("dist material must hold N/nranks planes")
+            idb = C.create_string_buffer(bytes(nid), 128)
+            _check(lib.gmt_create_dist(C.byref(cfg), ptr, dt, loc, rank, nranks, idb, C.byref(h)),
+                   "gmt_create_dist")
+        elif slabs > 1:
+            _check(lib.gmt_create_slabs(C.byref(cfg), ptr, dt, loc, slabs, C.byref(h)), "gmt_create_slabs")
+        else:
+            _check(lib.gmt_create(C.byref(cfg), ptr, dt, loc, C.byref(h)), "gmt_create")
         self._h = h
+        self.nz = nz   # planes held at level 0 (N, or N/P for dist)
         self.lib = lib
         self.physics = physics
         self.n = n
@@ -193,7 +231,13 @@ class Problem:
 
     def vec_shape(self, level: int = 0):
         n = self.level_res(level)
+        if level == 0:
+            return (self.nrhs, self.dpn, self.nz, n, n)
         return (self.nrhs, self.dpn, n, n, n)
+
+    @property
+    def num_slabs(self) -> int:
+        return self.lib.gmt_num_slabs(self._h)
 
     @property
     def stream(self) -> int:
