@@ -210,29 +210,33 @@ def batch_truss_psl(n: int, count: int, seed: int = 0):
 
 
 def initial_guess(n: int, nrhs: int, dpn: int, seed: int = 0, amp: float = 0.1,
-                  material: np.ndarray | None = None) -> np.ndarray:
+                  material: np.ndarray | None = None, z0: int = 0, nz: int | None = None) -> np.ndarray:
     """A smooth, seeded synthetic warm start u_hat^1 (Alg. 2 line 1 input),
     layout [m, c, z, y, x] float32 (component planes); zero on nodes whose 8
-    surrounding voxels are all void when ``material`` is given.  Stands in
-    for the network prediction, which is out of scope."""
+    surrounding voxels are all void when ``material`` (the full N^3 field) is
+    given.  Stands in for the network prediction, which is out of scope.
+    z0/nz select the planes [z0, z0+nz) of the same field (a rank's slab)."""
+    nz = n - z0 if nz is None else nz
     rng = np.random.default_rng(seed)
     t = _axes(n)
-    out = np.zeros((nrhs, dpn, n, n, n), dtype=np.float32)
+    tz = t[z0:z0 + nz]
+    out = np.zeros((nrhs, dpn, nz, n, n), dtype=np.float32)
     for m in range(nrhs):
         for c in range(dpn):
             a = rng.standard_normal(3)
             ph = rng.uniform(0, _TWO_PI, 3)
             fx = np.sin(_TWO_PI * t + ph[0]) * a[0]
             fy = np.sin(_TWO_PI * t + ph[1]) * a[1]
-            fz = np.sin(_TWO_PI * t + ph[2]) * a[2]
+            fz = np.sin(_TWO_PI * tz + ph[2]) * a[2]
             out[m, c] = amp * (fz[:, None, None] + fy[None, :, None] + fx[None, None, :])
     if material is not None:
-        occ = material > 0
-        act = np.zeros_like(occ)
+        # node (z, y, x) touches voxels z-1..z, y-1..y, x-1..x (periodic)
+        occ = np.take(material > 0, np.arange(z0 - 1, z0 + nz) % n, axis=0)
+        act = np.zeros((nz, n, n), dtype=bool)
         for dz in (0, 1):
             for dy in (0, 1):
                 for dx in (0, 1):
-                    act |= np.roll(occ, shift=(dz, dy, dx), axis=(0, 1, 2))
+                    act |= np.roll(occ, shift=(dy, dx), axis=(1, 2))[1 - dz:1 - dz + nz]
         out[:, :, ~act] = 0.0
     return out
 

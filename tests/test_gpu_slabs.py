@@ -143,3 +143,11 @@ def test_slab_errors():
             B.gmt_inject_correction(1, np.zeros(B.vec_shape(1), np.float32))
     with pytest.raises(GmtError):            # 16 / 4 = 4 planes: < 3 partitioned levels
         _problem(synth.tpms(16, "gyroid", 0.3), "elastic", 3, slabs=4)
+
+
+def test_nccl_loads_and_makes_unique_id():
+    """The NCCL transport dlopens libnccl.so.2 (torch's copy when torch is
+    loaded) and creates the id rank 0 broadcasts to gmt_create_dist."""
+    from paper_2604_26518_b200 import gmt
+    a, b = gmt.gmt_nccl_unique_id(), gmt.gmt_nccl_unique_id()
+    assert len(a) == 128 and a != bytes(128) and a != b
