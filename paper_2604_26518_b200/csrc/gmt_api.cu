@@ -248,6 +248,20 @@ struct Prof {
 
 // ---------------------------------------------------------------- launches
 
+// One resident wave of the C^H kernel (grid-stride inside).
+template <int DPN>
+int ch_grid() {
+  static int g = 0;
+  if (!g) {
+    int per = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_effective_tensor<DPN>, CH_THREADS, 0);
+    g = std::max(1, per) * std::max(1, sms);
+  }
+  return g;
+}
+
 template <int DPN>
 int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part,
               int skip_void = 0) {
@@ -560,10 +574,10 @@ template <int DPN>
 int effective_tensor(gmt_problem p, const float* u, double* CH) {
   constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
   const LevelBuf& b = p->lv[0];
-  const int nblk = std::max(1, (p->ecount + 127) / 128);
+  const int nblk = std::max(1, std::min((p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
   {
     Prof prof(p, 7);
-    k_effective_tensor<DPN><<<nblk, 128, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
+    k_effective_tensor<DPN><<<nblk, CH_THREADS, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
                                                          (float)p->ed.mu, p->part, b.cs, p->elist,
                                                          p->ecount);
     LAUNCHED(p);
@@ -750,6 +764,11 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   p->fc.lam = (float)p->ed.lam;
   p->fc.mu = (float)p->ed.mu;
   p->fc.omega = (float)cfg.omega;
+  for (int q = 0; q < 3; ++q) {
+    const int dq = q < p->ed.dpn ? q : 0;
+    const double hpp = p->ed.H[13 * 9 + dq * p->ed.dpn + dq];   // ElementData::H is [d][9]
+    p->fc.wd[q] = (float)(cfg.omega / hpp);
+  }
   std::vector<float> m1(8 * nd * nd);
   for (int j = 0; j < 8; ++j)
     for (int i = 0; i < nd * nd; ++i) m1[j * nd * nd + i] = (float)p->ed.M1[j][i];

@@ -41,6 +41,7 @@ struct CoarseH {         // homogeneous Galerkin stencil of one coarse level (c 
 struct FineConsts {      // level 0 (material-driven) operator: material scalars
   float lam, mu;         // Lame constants (elastic) / kappa in lam (heat)
   float omega;           // damped-Jacobi factor
+  float wd[3];           // omega / H_pp: Jacobi weight of a uniform node of scale 1 (divide by c)
 };
 
 // Block-wide reduction of NV doubles per thread; thread 0 of the block

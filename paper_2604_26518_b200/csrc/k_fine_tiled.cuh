@@ -57,8 +57,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // COARSE: level >= 1 -- uniform nodes use c H_l from the kernel parameter HP
 // (direct form; coarse vectors are corrections), and the right-hand side f is
 // read from memory (the restricted residual) instead of being zero.
+#ifndef TT_MINB
+#define TT_MINB 5
+#endif
 template <int DPN, int MODE, int NRG, bool COARSE = false>
-__global__ void __launch_bounds__(TT_X * TT_Y)
+__global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB)
 k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
              float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
              ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty,
@@ -82,29 +85,49 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const bool vec_rows = (x0 + TT_X <= n) && ((n & 3) == 0) && ((cs & 3) == 0);
 
-  // tile flags of voxel planes z0-3 .. z0+ZC+1 loaded once into a bitmask
-  unsigned long long fm = 0ull;
-  for (int i = 0; i < TT_ZC + 5; ++i)
-    if (flag[((ptrdiff_t)zs(z0 - 3 + i) * nty + blockIdx.y) * ntx + blockIdx.x]) fm |= 1ull << i;
-  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1ull; };
+  // tile flags of voxel planes z0-3 .. z0+ZC+1: one flag per lane, one ballot
+  static_assert(TT_ZC + 5 <= 32, "flag window must fit a warp");
+  const int lane = tid & 31;
+  const bool fl_on = lane < TT_ZC + 5 &&
+                     flag[((ptrdiff_t)zs(z0 - 3 + lane) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
+  const unsigned fm = __ballot_sync(0xffffffffu, fl_on);
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1u; };
   auto needed = [&](int p) -> bool {   // node plane p read by some active node of planes p-1..p+1
-    return vflag(p - 2) || vflag(p - 1) || vflag(p) || vflag(p + 1);
+    return (fm >> (p - z0 + 1)) & 0xfu;
   };
+  // staging assignments are the same for every plane: precompute per thread
+  // the interior 16-byte chunks (V x TT_PY rows x 8) and the halo floats
+  constexpr int NCH = V * TT_PY * 8, NHA = V * TT_PY * 2;
+  constexpr int CPT = (NCH + NTH - 1) / NTH;
+  static_assert(NHA <= NTH, "one halo float per thread");
+  ptrdiff_t c_src[CPT];
+  int c_dst[CPT];
+  ptrdiff_t h_src = 0;
+  int h_dst = -1;
+  if (vec_rows) {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int q = tid + i * NTH;
+      const int k = q / (TT_PY * 8), rem = q - k * (TT_PY * 8);
+      const int py = rem / 8, c = rem - py * 8;
+      c_src[i] = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + x0 + 4 * c;
+      c_dst[i] = q < NCH ? k * TT_PLS + py * TT_RS + 4 + 4 * c : -1;
+    }
+    if (tid < NHA) {
+      const int k = tid / (TT_PY * 2), rem = tid - k * (TT_PY * 2);
+      const int py = rem >> 1, side = rem & 1;
+      h_src = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + wrapi(side ? x0 + TT_X : x0 - 1, n);
+      h_dst = k * TT_PLS + py * TT_RS + (side ? 4 + TT_X : 3);
+    }
+  }
   auto issue = [&](int p) {            // stage node plane p into slot p % NB
     float* dst = smem + (size_t)((p + 2 * TT_NB) % TT_NB) * V * TT_PLS;
     const float* src = u + (ptrdiff_t)zu(p) * plane;
     if (vec_rows) {
-      // per (component, row): 8 x 16-byte interior chunks + 2 halo floats
-      for (int q = tid; q < V * TT_PY * 10; q += NTH) {
-        const int k = q / (TT_PY * 10), rem = q - k * (TT_PY * 10);
-        const int py = rem / 10, c = rem - py * 10;
-        const int gy = wrapi(y0 - 1 + py, n);
-        const float* row = src + k * cs + (ptrdiff_t)gy * n;
-        float* drow = dst + k * TT_PLS + py * TT_RS;
-        if (c < 8) cp_async16(drow + 4 + 4 * c, row + x0 + 4 * c);
-        else if (c == 8) cp_async4(drow + 3, row + wrapi(x0 - 1, n));
-        else cp_async4(drow + 4 + TT_X, row + wrapi(x0 + TT_X, n));
-      }
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+        if (c_dst[i] >= 0) cp_async16(dst + c_dst[i], src + c_src[i]);
+      if (h_dst >= 0) cp_async4(dst + h_dst, src + h_src);
     } else {
       for (int q = tid; q < V * TT_PY * (TT_X + 2); q += NTH) {
         const int k = q / (TT_PY * (TT_X + 2)), rem = q - k * (TT_PY * (TT_X + 2));
@@ -176,16 +199,23 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
           const float* f = f_all + (ptrdiff_t)grp * V * cs;
 #pragma unroll
           for (int k = 0; k < V; ++k) fl[k] = __ldg(f + k * cs + node);
+          op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr,
+                                      grp * NRG);
         } else {
           node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
+          const float rc = __frcp_rn(c);
+          float Dinv[DPN];
+#pragma unroll
+          for (int p = 0; p < DPN; ++p) Dinv[p] = P.wd[p] * rc;
+          op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr,
+                                      grp * NRG, Dinv);
         }
-        op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr, grp * NRG);
       }
     }
     __syncthreads();
   }
   cp_async_wait<0>();
-  if (part) {
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
     const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
   }
@@ -306,7 +336,7 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
     __syncthreads();
   }
   cp_async_wait<0>();
-  if (part) {
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
     const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
   }

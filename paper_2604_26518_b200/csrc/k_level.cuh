@@ -36,9 +36,13 @@ __device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp
                                             const float (&acc)[NRG * DPN], const float (&fl)[NRG * DPN],
                                             const float (&ui)[NRG * DPN], const float (&D)[DPN],
                                             float omega, double (&nrm)[2 * Tr<DPN>::NR], bool want_nrm,
-                                            int m0 = 0) {
+                                            int m0 = 0, const float* Dinv_pre = nullptr) {
   constexpr int NR = Tr<DPN>::NR, V = NRG * DPN;
   float o[V];
+  // omega / D once per component (Dinv_pre: supplied by the caller)
+  float Dinv[DPN];
+#pragma unroll
+  for (int p = 0; p < DPN; ++p) Dinv[p] = Dinv_pre ? Dinv_pre[p] : (D[p] > 0.f ? omega / D[p] : 0.f);
 #pragma unroll
   for (int m = 0; m < NRG; ++m)
 #pragma unroll
@@ -48,7 +52,7 @@ __device__ __forceinline__ void op_epilogue(bool valid, float* __restrict__ outp
       if (MODE == M_APPLY) o[k] = acc[k];
       else if (MODE == M_RESID) o[k] = r;
       else if (MODE == M_LOADS) o[k] = fl[k];
-      else /* M_JACOBI */ o[k] = D[p] > 0.f ? fmaf(omega / D[p], r, ui[k]) : ui[k];
+      else /* M_JACOBI */ o[k] = fmaf(Dinv[p], r, ui[k]);
       if ((MODE == M_RESID || MODE == M_JACOBI) && want_nrm && valid) {
         if (NRG == NR) {
           nrm[m] += (double)r * (double)r;
