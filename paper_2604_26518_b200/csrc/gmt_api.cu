@@ -272,11 +272,12 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = b.cs;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
-    const bool packed = DPN == 3 && p->variant == 1;
-    const int NRG = DPN == 3 ? (packed ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
+    const bool packed = DPN == 3 && p->variant == 1, pairs = DPN == 3 && (p->variant == 2 || p->variant == 4);
+    const bool zb = p->variant == 3 || p->variant == 4;
+    const int NRG = DPN == 3 ? (packed || pairs ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
     const ZMap z = p->zm(0);
     const dim3 grid(p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
-    const size_t shm = (size_t)TT_NB * NRG * DPN * TT_PLS * sizeof(float);
+    const size_t shm = (size_t)(zb ? TT_NB2 : TT_NB) * NRG * DPN * TT_PLS * sizeof(float);
     const int nbt = grid.x * grid.y * grid.z;
     double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
     const int nbi = (p->icount + 127) / 128;
@@ -287,6 +288,29 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
       else
         k_fine_tiled2<M_RESID><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
                                                          p->tntx, p->tnty);
+    } else if (zb) {
+      if (pairs) {
+        if (mode == M_JACOBI)
+          k_fine_tiled_zb<3, M_JACOBI, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                    cs, p->tflag, p->tntx, p->tnty);
+        else
+          k_fine_tiled_zb<3, M_RESID, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                   cs, p->tflag, p->tntx, p->tnty);
+      } else {
+        if (mode == M_JACOBI)
+          k_fine_tiled_zb<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc,
+                                                                      part, cs, p->tflag, p->tntx, p->tnty);
+        else
+          k_fine_tiled_zb<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc,
+                                                                     part, cs, p->tflag, p->tntx, p->tnty);
+      }
+    } else if (pairs) {
+      if (mode == M_JACOBI)
+        k_fine_tiled<3, M_JACOBI, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                               p->tflag, p->tntx, p->tnty);
+      else
+        k_fine_tiled<3, M_RESID, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
+                                                              p->tflag, p->tntx, p->tnty);
     } else {
       if (mode == M_JACOBI)
         k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
@@ -602,7 +626,7 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
   // of the tiled kernel followed by those of the interface kernel
   TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
-  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (DPN == 3 ? (p->variant == 1 ? 3 : 2) : 1) +
+  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (DPN == 3 ? (p->variant == 1 || p->variant == 2 || p->variant == 4 ? 3 : 2) : 1) +
                     (p->icount + 127) / 128,
              2 * NR));
   for (int m = 0; m < NR; ++m) {
@@ -883,6 +907,8 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     const int shm2 = TT_NB * 6 * TT_PLS * (int)sizeof(float);
     const int shm3 = TT_NB * 9 * TT_PLS * (int)sizeof(float);
     const int shm1 = TT_NB * 3 * TT_PLS * (int)sizeof(float);
+    const int shm3z = TT_NB2 * 9 * TT_PLS * (int)sizeof(float), shm2z = TT_NB2 * 6 * TT_PLS * (int)sizeof(float);
+    const int shm1z = TT_NB2 * 3 * TT_PLS * (int)sizeof(float);
     if (cudaFuncSetAttribute(k_fine_tiled2<M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled2<M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
@@ -892,7 +918,13 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1))
+        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3z) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3z) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_RESID, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z) ||
+        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z))
       return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
   }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);

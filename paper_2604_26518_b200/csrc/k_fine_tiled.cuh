@@ -60,6 +60,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef TT_MINB
 #define TT_MINB 5
 #endif
+#ifndef TT_MINB2
+#define TT_MINB2 3
+#endif
 template <int DPN, int MODE, int NRG, bool COARSE = false>
 __global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB)
 k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
@@ -202,7 +205,8 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
           op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr,
                                       grp * NRG);
         } else {
-          node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
+          if constexpr (DPN == 3 && NRG == 2) node_uniform_pk(get, c, P.lam, P.mu, ui, acc, D);
+          else node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
           const float rc = __frcp_rn(c);
           float Dinv[DPN];
 #pragma unroll
@@ -221,12 +225,165 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
   }
 }
 
+// Level-0 sweep computing two z-planes per step ("z-blocking"): each thread
+// owns the nodes (x, y, z) and (x, y, z+1).  Their 27-point neighbourhoods
+// share 18 positions, so one step reads 4 staged planes for 2 nodes instead
+// of 3 per node (shared-memory traffic -1/3; the loads of the shared planes
+// are common subexpressions of the two node_uniform calls) and the ring of
+// TT_NB2 = 6 slots needs one barrier pair per two planes.
+constexpr int TT_NB2 = 6;
+template <int DPN, int MODE, int NRG>
+__global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB2)
+k_fine_tiled_zb(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
+                float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
+                ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
+  static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = NRG * DPN, NG = NR / NRG, NB = TT_NB2;
+  const int grp = blockIdx.z % NG, chunk = blockIdx.z / NG;
+  const float* __restrict__ u = u_all + (ptrdiff_t)grp * V * cs;
+  float* __restrict__ out = out_all + (ptrdiff_t)grp * V * cs;
+  constexpr int NTH = TT_X * TT_Y;
+  extern __shared__ __align__(16) float smem[];   // [NB][V][TT_PY][TT_RS]
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TT_X + tx;
+  const int x0 = blockIdx.x * TT_X, y0 = blockIdx.y * TT_Y;
+  const int z0 = chunk * TT_ZC, z1 = min(nz, z0 + TT_ZC);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = (x < n) && (y < n);
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  const bool vec_rows = (x0 + TT_X <= n) && ((n & 3) == 0) && ((cs & 3) == 0);
+
+  const int lane = tid & 31;
+  const bool fl_on = lane < TT_ZC + 5 &&
+                     flag[((ptrdiff_t)zs(z0 - 3 + lane) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
+  const unsigned fm = __ballot_sync(0xffffffffu, fl_on);
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1u; };
+  auto needed = [&](int p) -> bool { return (fm >> (p - z0 + 1)) & 0xfu; };
+  constexpr int NCH = V * TT_PY * 8, NHA = V * TT_PY * 2;
+  constexpr int CPT = (NCH + NTH - 1) / NTH;
+  static_assert(NHA <= NTH, "one halo float per thread");
+  ptrdiff_t c_src[CPT];
+  int c_dst[CPT];
+  ptrdiff_t h_src = 0;
+  int h_dst = -1;
+  if (vec_rows) {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int q = tid + i * NTH;
+      const int k = q / (TT_PY * 8), rem = q - k * (TT_PY * 8);
+      const int py = rem / 8, c = rem - py * 8;
+      c_src[i] = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + x0 + 4 * c;
+      c_dst[i] = q < NCH ? k * TT_PLS + py * TT_RS + 4 + 4 * c : -1;
+    }
+    if (tid < NHA) {
+      const int k = tid / (TT_PY * 2), rem = tid - k * (TT_PY * 2);
+      const int py = rem >> 1, side = rem & 1;
+      h_src = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + wrapi(side ? x0 + TT_X : x0 - 1, n);
+      h_dst = k * TT_PLS + py * TT_RS + (side ? 4 + TT_X : 3);
+    }
+  }
+  auto slot = [&](int p) -> float* { return smem + (size_t)((p + 2 * NB) % NB) * V * TT_PLS; };
+  auto issue = [&](int p) {
+    float* dst = slot(p);
+    const float* src = u + (ptrdiff_t)zu(p) * plane;
+    if (vec_rows) {
+#pragma unroll
+      for (int i = 0; i < CPT; ++i)
+        if (c_dst[i] >= 0) cp_async16(dst + c_dst[i], src + c_src[i]);
+      if (h_dst >= 0) cp_async4(dst + h_dst, src + h_src);
+    } else {
+      for (int q = tid; q < V * TT_PY * (TT_X + 2); q += NTH) {
+        const int k = q / (TT_PY * (TT_X + 2)), rem = q - k * (TT_PY * (TT_X + 2));
+        const int py = rem / (TT_X + 2), px = rem - py * (TT_X + 2);
+        const int gy = wrapi(y0 - 1 + py, n), gx = wrapi(x0 - 1 + px, n);
+        cp_async4(dst + k * TT_PLS + py * TT_RS + 3 + px, src + k * cs + (ptrdiff_t)gy * n + gx);
+      }
+    }
+  };
+
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+  // prologue: planes z0-1 .. z0+2 (the first step's window), one group each
+  for (int p = z0 - 1; p <= z0 + 2; ++p) {
+    if (p <= z1 && needed(p)) issue(p);
+    cp_async_commit();
+  }
+  const float* code_col = code + (ptrdiff_t)yc * n + xc;
+  float cn0 = valid ? __ldg(code_col + (ptrdiff_t)z0 * plane) : 0.f;
+  float cn1 = (valid && z0 + 1 < z1) ? __ldg(code_col + (ptrdiff_t)(z0 + 1) * plane) : 0.f;
+  const int base = (ty + 1) * TT_RS + 4 + tx;
+  for (int z = z0; z < z1; z += 2) {
+    const float c0 = cn0, c1 = cn1;
+    if (z + 2 < z1) cn0 = valid ? __ldg(code_col + (ptrdiff_t)(z + 2) * plane) : 0.f;
+    if (z + 3 < z1) cn1 = valid ? __ldg(code_col + (ptrdiff_t)(z + 3) * plane) : 0.f;
+#pragma unroll
+    for (int j = 3; j <= 4; ++j) {   // next step's new planes
+      if (z + j <= z1 && needed(z + j)) issue(z + j);
+      cp_async_commit();
+    }
+    cp_async_wait<2>();
+    __syncthreads();
+    const bool act0 = vflag(z - 1) || vflag(z), act1 = z + 1 < z1 && (vflag(z) || vflag(z + 1));
+    const bool u0 = act0 && c0 > 0.f, u1 = act1 && c1 > 0.f;
+    if (u0 || u1) {
+      const float* sl[4];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) sl[d] = slot(z - 1 + d);
+      auto get0 = [&](int dx, int dy, int dz, int k) -> float {
+        return sl[dz + 1][k * TT_PLS + base + dy * TT_RS + dx];
+      };
+      auto get1 = [&](int dx, int dy, int dz, int k) -> float {
+        return sl[dz + 2][k * TT_PLS + base + dy * TT_RS + dx];
+      };
+      float acc0[V], acc1[V], fl[V], ui0[V], ui1[V], D0[DPN], D1[DPN];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        fl[k] = 0.f;
+        ui0[k] = get0(0, 0, 0, k);
+        ui1[k] = get1(0, 0, 0, k);
+      }
+      const float cc0 = u0 ? c0 : 1.f, cc1 = u1 ? c1 : 1.f;   // finite scales for lanes not stored
+      if constexpr (DPN == 3 && NRG == 2) {
+        node_uniform_pk(get0, cc0, P.lam, P.mu, ui0, acc0, D0);
+        node_uniform_pk(get1, cc1, P.lam, P.mu, ui1, acc1, D1);
+      } else {
+        node_uniform<DPN, NRG>(get0, cc0, P.lam, P.mu, ui0, acc0, D0);
+        node_uniform<DPN, NRG>(get1, cc1, P.lam, P.mu, ui1, acc1, D1);
+      }
+      float Dinv0[DPN], Dinv1[DPN];
+      const float r0 = __frcp_rn(cc0), r1 = __frcp_rn(cc1);
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) {
+        Dinv0[p] = P.wd[p] * r0;
+        Dinv1[p] = P.wd[p] * r1;
+      }
+      const ptrdiff_t node = (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc;
+      if (u0)
+        op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc0, fl, ui0, D0, P.omega, nrm, part != nullptr,
+                                    grp * NRG, Dinv0);
+      if (u1)
+        op_epilogue<DPN, MODE, NRG>(valid, out + node + plane, cs, acc1, fl, ui1, D1, P.omega, nrm,
+                                    part != nullptr, grp * NRG, Dinv1);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
 // Elasticity variant processing load cases in pairs with packed FP32x2
 // arithmetic (FADD2/FFMA2): CTA group g handles load cases (2g, 2g+1); its
 // shared-memory slots interleave the pair, [c][row][x][2], so one LDS.64 gives
 // a packed operand.  Same algebra as node_uniform (difference form, c H(d)).
 template <int MODE>
-__global__ void __launch_bounds__(TT_X * TT_Y)
+__global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB)
 k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
               float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
               ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty) {
@@ -247,22 +404,35 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
   const int xc = valid ? x : 0, yc = valid ? y : 0;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
 
-  // tile flags of voxel planes z0-3 .. z0+ZC+1 loaded once into a bitmask
-  unsigned long long fm = 0ull;
-  for (int i = 0; i < TT_ZC + 5; ++i)
-    if (flag[((ptrdiff_t)zs(z0 - 3 + i) * nty + blockIdx.y) * ntx + blockIdx.x]) fm |= 1ull << i;
-  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1ull; };
-  auto needed = [&](int p) -> bool { return vflag(p - 2) || vflag(p - 1) || vflag(p) || vflag(p + 1); };
+  // tile flags of voxel planes z0-3 .. z0+ZC+1: one flag per lane, one ballot
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool fl_on = lane < TT_ZC + 5 &&
+                     flag[((ptrdiff_t)zs(z0 - 3 + lane) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
+  const unsigned fm = __ballot_sync(0xffffffffu, fl_on);
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1u; };
+  auto needed = [&](int p) -> bool { return (fm >> (p - z0 + 1)) & 0xfu; };
+  // staging: rows (c, py, j) of TT_X + 2 floats; warp w copies rows w, w+4, ...
+  // (lane -> x0-1+lane, lanes 0/1 also the two right-most columns); the row
+  // offsets are plane-independent and precomputed
+  constexpr int NROW = DPN * TT_PY * 2, RPW = NROW / (NTH / 32);
+  static_assert(NROW % (NTH / 32) == 0, "rows per warp");
+  ptrdiff_t r_src[RPW];
+  int r_dst[RPW];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + i * (NTH / 32);
+    const int j = r & 1, cp = r >> 1, c = cp / TT_PY, py = cp - c * TT_PY;
+    r_src[i] = (ptrdiff_t)(j * DPN + c) * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n;
+    r_dst[i] = ((c * TT_PY + py) * TT_RS + 3) * 2 + j;
+  }
+  const int gx0 = wrapi(x0 - 1 + lane, n), gx1 = wrapi(x0 + 31 + lane, n);
   auto issue = [&](int p) {
     float* dst = smem + (size_t)((p + 2 * TT_NB) % TT_NB) * SLOT;
     const float* src = u + (ptrdiff_t)zu(p) * plane;
-    constexpr int PX = TT_X + 2;
-    for (int q = tid; q < DPN * TT_PY * PX * 2; q += NTH) {
-      const int j = q & 1, r = q >> 1;
-      const int c = r / (TT_PY * PX), rem = r - c * (TT_PY * PX);
-      const int py = rem / PX, px = rem - py * PX;
-      const int gy = wrapi(y0 - 1 + py, n), gx = wrapi(x0 - 1 + px, n);
-      cp_async4(dst + ((c * TT_PY + py) * TT_RS + 3 + px) * 2 + j, src + (j * DPN + c) * cs + (ptrdiff_t)gy * n + gx);
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      cp_async4(dst + r_dst[i] + 2 * lane, src + r_src[i] + gx0);
+      if (lane < 2) cp_async4(dst + r_dst[i] + 2 * (32 + lane), src + r_src[i] + gx1);
     }
   };
   // combined homogeneous stencil values h = lam Hl + mu Hm, packed (h, h);
@@ -320,17 +490,18 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
             }
         }
         // unpack (load case 2g, 2g+1) and reuse the scalar epilogue
-        float a[6], fl[6], uu[6], D[DPN];
+        float a[6], fl[6], uu[6], D[DPN], Dinv[DPN];
+        const float rc = __frcp_rn(c);
 #pragma unroll
         for (int cc = 0; cc < DPN; ++cc) {
           upk2(mul2(acc[cc], pk2(c, c)), a[cc], a[3 + cc]);
           upk2(ui[cc], uu[cc], uu[3 + cc]);
           fl[cc] = fl[3 + cc] = 0.f;
-          const int i = 13 * 9 + cc * 3 + cc;
-          D[cc] = c * fmaf(P.lam, CT<3>::Hl(i), P.mu * CT<3>::Hm(i));
+          D[cc] = 0.f;
+          Dinv[cc] = P.wd[cc] * rc;
         }
         op_epilogue<DPN, MODE, 2>(valid, out + (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc, cs, a, fl, uu, D,
-                                  P.omega, nrm, part != nullptr, grp * 2);
+                                  P.omega, nrm, part != nullptr, grp * 2, Dinv);
       }
     }
     __syncthreads();

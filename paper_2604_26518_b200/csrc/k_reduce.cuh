@@ -3,6 +3,7 @@
 #pragma once
 
 #include "gmt_common.cuh"
+#include "f32x2.cuh"
 
 namespace gmt {
 
@@ -37,18 +38,20 @@ k_reduce_stage(const double* __restrict__ part, int nblk, int nv, double* __rest
 //   sum_g w_g (e_m - eps_g(u^m)) : C_0 : (e_n - eps_g(u^n)).
 // Gradients come from nodal differences along the element edges (exact in fp32
 // even when |u| ~ N): d u / d x_r is constant along r and bilinear in the two
-// transverse coordinates, so its 8 Gauss values are a 2x2 interpolation of the
-// 4 r-edge differences (separable, 16 flops instead of 56).  The Gauss points
-// are taken in two halves (z = G0, G1) so that the strains of all load cases
-// at 4 points are staged in shared memory (thread-fastest, conflict-free)
-// for the NR(NR+1)/2 Gram sums; isotropic C_0
-// gives sigma = lam tr(eps) I + 2 mu eps (thermal: q = kappa grad, lam carries
-// kappa).  Grid-stride over the active-element list; per-element fp32 sums are
-// accumulated in fp64 per thread, then one block partial of the upper triangle.
+// transverse coordinates, so its 8 Gauss values are a separable 2x2
+// interpolation of the 4 r-edge differences.  The Gauss points are processed
+// as (z-half, y) rows of two points (x = G0, G1) held as packed FP32 pairs
+// (FADD2/FFMA2/FMUL2): d/dx is equal in both, d/dy and d/dz differ.  The
+// strains of all load cases of a half are staged in shared memory
+// (thread-fastest float2, conflict-free) for the NR(NR+1)/2 Gram sums;
+// isotropic C_0 gives sigma = lam tr(eps) I + 2 mu eps (thermal: q = kappa
+// grad, lam carries kappa).  Grid-stride over the active-element list;
+// per-element fp32 sums are accumulated in fp64 per thread, then one block
+// partial of the upper triangle.
 constexpr int CH_THREADS = 64;
 
 template <int DPN>
-__global__ void __launch_bounds__(CH_THREADS)
+__global__ void __launch_bounds__(CH_THREADS, 6)
 k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMap zu, int n, int nz,
                    float lam, float mu, double* __restrict__ part, ptrdiff_t cs,
                    const int* __restrict__ elist, int ecount) {
@@ -59,143 +62,121 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
   constexpr float G0 = 0.21132486540518713f;  // (1 - 1/sqrt(3)) / 2
   constexpr float G1 = 0.78867513459481287f;  // (1 + 1/sqrt(3)) / 2
   const ptrdiff_t plane = (ptrdiff_t)n * n;
-  __shared__ float Esh[NR * 4 * NE][CH_THREADS];   // e_m - eps(u^m) at (gx, gy) = (g & 1, g >> 1), z = gz
-#define ESH(m, g, i) Esh[((m) * 4 + (g)) * NE + (i)][threadIdx.x]
+  // e_m - eps(u^m) at the Gauss pair (gy, x = G0|G1) of the current z-half
+  __shared__ f2 Esh[NR * 2 * NE][CH_THREADS];
+  const f2 Gp = pk2(G0, G1);
+  const f2 two_mu = pk2(2.f * mu, 2.f * mu), lam2 = pk2(lam, lam), mu2 = pk2(mu, mu);
   double q[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) q[k] = 0.0;
-  // software pipeline: the corner values of the next (element, half, load
-  // case) round are in flight while the current round is processed
-  const int stride = gridDim.x * blockDim.x;
-  int it = blockIdx.x * blockDim.x + threadIdx.x;
-  int offc[8], offn[8];   // within one component plane (n^2 * planes < 2^31)
-  float sec = 0.f, sen = 0.f;
-  auto meta = [&](int i, int(&o)[8], float& se) {
-    const ptrdiff_t eid = __ldg(elist + i);
-    se = __ldg(s + eid);
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < ecount; it += gridDim.x * blockDim.x) {
+    const ptrdiff_t eid = __ldg(elist + it);
+    const float se = __ldg(s + eid);
     const int x = (int)(eid % n), y = (int)((eid / n) % n), z = (int)(eid / plane);
+    unsigned off[8];   // within one component plane (< 2^32 floats)
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      o[k] = (int)((ptrdiff_t)zu(z + (k >> 2)) * plane + (ptrdiff_t)wrapi(y + ((k >> 1) & 1), n) * n +
-                   wrapi(x + (k & 1), n));
-  };
-  float cur[DPN][8], nxt[DPN][8];
-  auto fetch = [&](const int(&o)[8], int m, float(&d)[DPN][8]) {
+      off[k] = (unsigned)((ptrdiff_t)zu(z + (k >> 2)) * plane + (ptrdiff_t)wrapi(y + ((k >> 1) & 1), n) * n +
+                          wrapi(x + (k & 1), n));
+    f2 qf[NQ];
 #pragma unroll
-    for (int c = 0; c < DPN; ++c) {
-      const float* uc = u + (ptrdiff_t)(m * DPN + c) * cs;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) d[c][k] = __ldg(uc + o[k]);
-    }
-  };
-  if (it < ecount) {
-    meta(it, offc, sec);
-    fetch(offc, 0, cur);
-  }
-  for (; it < ecount; it += stride) {
-    const bool has_next = it + stride < ecount;
-    if (has_next) meta(it + stride, offn, sen);
-    float qf[NQ];
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) qf[k] = 0.f;
+    for (int k = 0; k < NQ; ++k) qf[k] = 0ull;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const float gz = h ? G1 : G0;
-#pragma unroll 1
+#pragma unroll 3
       for (int m = 0; m < NR; ++m) {
-        if (m + 1 < NR) fetch(offc, m + 1, nxt);
-        else if (h == 0) fetch(offc, 0, nxt);
-        else if (has_next) fetch(offn, 0, nxt);
-        float gr[4][3][DPN];   // gr[g][r][c] = d u_c / d x_r
+        f2 gxv[2][DPN], gyv[DPN], gzv[2][DPN];   // [gy][c] pairs over x = G0, G1
 #pragma unroll
         for (int c = 0; c < DPN; ++c) {
-          const float(&uc)[8] = cur[c];
-          // x-edges (y = j, z = k) -> z = gz -> y = gy
+          const float* bp = u + (ptrdiff_t)(m * DPN + c) * cs;
+          float uc[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) uc[k] = __ldg(bp + off[k]);
           float ax[2], ay[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < 2; ++j) {   // x-edges (y = j), interpolated to z = gz
             const float d0 = uc[1 + 2 * j] - uc[2 * j], d1 = uc[5 + 2 * j] - uc[4 + 2 * j];
             ax[j] = fmaf(gz, d1 - d0, d0);
           }
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {   // y-edges (x = i, z = k)
+          for (int i = 0; i < 2; ++i) {   // y-edges (x = i), interpolated to z = gz
             const float d0 = uc[2 + i] - uc[i], d1 = uc[6 + i] - uc[4 + i];
             ay[i] = fmaf(gz, d1 - d0, d0);
           }
-          float dz[4];   // z-edges (x = i, y = j), index i + 2 j
-#pragma unroll
-          for (int k = 0; k < 4; ++k) dz[k] = uc[4 + k] - uc[k];
-          const float tx = ax[1] - ax[0], ty = ay[1] - ay[0];
-          const float zy0 = fmaf(G0, dz[1] - dz[0], dz[0]), zy1 = fmaf(G1, dz[1] - dz[0], dz[0]);   // y = 0
-          const float zt0 = fmaf(G0, dz[3] - dz[2], dz[2]), zt1 = fmaf(G1, dz[3] - dz[2], dz[2]);   // y = 1
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const float gx = (g & 1) ? G1 : G0, gy = (g >> 1) ? G1 : G0;
-            gr[g][0][c] = fmaf(gy, tx, ax[0]);
-            gr[g][1][c] = fmaf(gx, ty, ay[0]);
-            const float a0 = (g & 1) ? zy1 : zy0, a1 = (g & 1) ? zt1 : zt0;
-            gr[g][2][c] = fmaf(gy, a1 - a0, a0);
-          }
+          const float tx = ax[1] - ax[0];
+          gxv[0][c] = pk2(fmaf(G0, tx, ax[0]), fmaf(G0, tx, ax[0]));
+          gxv[1][c] = pk2(fmaf(G1, tx, ax[0]), fmaf(G1, tx, ax[0]));
+          gyv[c] = fma2(Gp, pk2(ay[1] - ay[0], ay[1] - ay[0]), pk2(ay[0], ay[0]));
+          // z-edges (x = i, y = j): pairs over x, then y = gy
+          const f2 dxy0 = sub2(pk2(uc[5] - uc[1], uc[5] - uc[1]), pk2(uc[4] - uc[0], uc[4] - uc[0]));
+          const f2 dxy1 = sub2(pk2(uc[7] - uc[3], uc[7] - uc[3]), pk2(uc[6] - uc[2], uc[6] - uc[2]));
+          const f2 a0 = fma2(Gp, dxy0, pk2(uc[4] - uc[0], uc[4] - uc[0]));   // y = 0 edge pair at x = G0, G1
+          const f2 a1 = fma2(Gp, dxy1, pk2(uc[6] - uc[2], uc[6] - uc[2]));   // y = 1
+          const f2 da = sub2(a1, a0);
+          gzv[0][c] = fma2(pk2(G0, G0), da, a0);
+          gzv[1][c] = fma2(pk2(G1, G1), da, a0);
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int gy = 0; gy < 2; ++gy) {
+          f2 E[NE];
           if constexpr (DPN == 3) {   // Voigt (11,22,33,23,13,12), engineering shear
-            ESH(m, g, 0) = (m == 0 ? 1.f : 0.f) - gr[g][0][0];
-            ESH(m, g, 1) = (m == 1 ? 1.f : 0.f) - gr[g][1][1];
-            ESH(m, g, 2) = (m == 2 ? 1.f : 0.f) - gr[g][2][2];
-            ESH(m, g, 3) = (m == 3 ? 1.f : 0.f) - (gr[g][2][1] + gr[g][1][2]);
-            ESH(m, g, 4) = (m == 4 ? 1.f : 0.f) - (gr[g][2][0] + gr[g][0][2]);
-            ESH(m, g, 5) = (m == 5 ? 1.f : 0.f) - (gr[g][1][0] + gr[g][0][1]);
+            E[0] = sub2(pk2(m == 0 ? 1.f : 0.f, m == 0 ? 1.f : 0.f), gxv[gy][0]);
+            E[1] = sub2(pk2(m == 1 ? 1.f : 0.f, m == 1 ? 1.f : 0.f), gyv[1]);
+            E[2] = sub2(pk2(m == 2 ? 1.f : 0.f, m == 2 ? 1.f : 0.f), gzv[gy][2]);
+            E[3] = sub2(pk2(m == 3 ? 1.f : 0.f, m == 3 ? 1.f : 0.f), add2(gzv[gy][1], gyv[2]));
+            E[4] = sub2(pk2(m == 4 ? 1.f : 0.f, m == 4 ? 1.f : 0.f), add2(gzv[gy][0], gxv[gy][2]));
+            E[5] = sub2(pk2(m == 5 ? 1.f : 0.f, m == 5 ? 1.f : 0.f), add2(gyv[0], gxv[gy][1]));
           } else {
-#pragma unroll
-            for (int r = 0; r < 3; ++r) ESH(m, g, r) = (m == r ? 1.f : 0.f) - gr[g][r][0];
+            E[0] = sub2(pk2(m == 0 ? 1.f : 0.f, m == 0 ? 1.f : 0.f), gxv[gy][0]);
+            E[1] = sub2(pk2(m == 1 ? 1.f : 0.f, m == 1 ? 1.f : 0.f), gyv[0]);
+            E[2] = sub2(pk2(m == 2 ? 1.f : 0.f, m == 2 ? 1.f : 0.f), gzv[gy][0]);
           }
+#pragma unroll
+          for (int i = 0; i < NE; ++i) Esh[(m * 2 + gy) * NE + i][threadIdx.x] = E[i];
         }
-#pragma unroll
-        for (int c = 0; c < DPN; ++c)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) cur[c][k] = nxt[c][k];
       }
 #pragma unroll 1
-      for (int g = 0; g < 4; ++g) {
-        float E[NR][NE];
+      for (int gy = 0; gy < 2; ++gy) {
+        f2 E[NR][NE];
 #pragma unroll
         for (int m = 0; m < NR; ++m)
 #pragma unroll
-          for (int i = 0; i < NE; ++i) E[m][i] = ESH(m, g, i);
+          for (int i = 0; i < NE; ++i) E[m][i] = Esh[(m * 2 + gy) * NE + i][threadIdx.x];
         int qi = 0;
 #pragma unroll
         for (int m = 0; m < NR; ++m) {
-          float sg[NE];
+          f2 sg[NE];
           if constexpr (DPN == 3) {
-            const float tr = E[m][0] + E[m][1] + E[m][2];
+            const f2 tr = add2(add2(E[m][0], E[m][1]), E[m][2]);
+            const f2 lt = mul2(lam2, tr);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) sg[i] = fmaf(2.f * mu, E[m][i], lam * tr);
+            for (int i = 0; i < 3; ++i) sg[i] = fma2(two_mu, E[m][i], lt);
 #pragma unroll
-            for (int i = 3; i < 6; ++i) sg[i] = mu * E[m][i];
+            for (int i = 3; i < 6; ++i) sg[i] = mul2(mu2, E[m][i]);
           } else {
 #pragma unroll
-            for (int i = 0; i < 3; ++i) sg[i] = lam * E[m][i];
+            for (int i = 0; i < 3; ++i) sg[i] = mul2(lam2, E[m][i]);
           }
 #pragma unroll
           for (int nn = m; nn < NR; ++nn) {
-            float a = qf[qi];
+            f2 a = qf[qi];
 #pragma unroll
-            for (int i = 0; i < NE; ++i) a = fmaf(sg[i], E[nn][i], a);
+            for (int i = 0; i < NE; ++i) a = fma2(sg[i], E[nn][i], a);
             qf[qi++] = a;
           }
         }
       }
     }
-    const double w = 0.125 * (double)sec;
+    const double w = 0.125 * (double)se;
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) q[k] = fma(w, (double)qf[k], q[k]);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) offc[k] = offn[k];
-    sec = sen;
+    for (int k = 0; k < NQ; ++k) {
+      float a, b;
+      upk2(qf[k], a, b);
+      q[k] = fma(w, (double)(a + b), q[k]);
+    }
   }
   block_reduce_store<NQ>(q, part + (ptrdiff_t)blockIdx.x * NQ);
-#undef ESH
 }
 
 // Sum of u over active nodes per (m, c) and the active-node count (level 0).
