@@ -138,9 +138,26 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(args, world: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
+    kernel from the committed `ncu --set full` capture (profiles/r1/traffic.json),
+    when it was taken on this exact single-GPU workload; else None."""
+    p = os.path.join(ROOT, "profiles", "r1", "traffic.json")
+    if world != 1 or not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh)
+    same = (d.get("res") == args.res and d.get("physics") == args.physics and d.get("geometry") == args.geometry
+            and abs(float(d.get("vf", -1)) - args.vf) < 1e-9 and args.levels in (0, 8))
+    return (float(d["dram_bytes_per_launch"]), d["source"]) if same else (None, None)
+
+
 # --------------------------------------------------------------------------- oracle leg
 
-def oracle_sample(physics: str, n_sample: int = 24, vf: float = 0.3):
+ORACLE_SAMPLE_N = 64   # configs[1]'s size: ~8 s of single-thread oracle work
+
+
+def oracle_sample(physics: str, n_sample: int = ORACLE_SAMPLE_N, vf: float = 0.3):
     """One step of the same workload run by the FP64 oracle on a bounded
     sample (an n_sample^3 gyroid, same generator and settings), single
     threaded.  Returns (seconds, sample description)."""
@@ -163,8 +180,8 @@ def oracle_sample(physics: str, n_sample: int = 24, vf: float = 0.3):
 
 
 def cpu_baseline(args):
-    dt, desc = oracle_sample(args.physics)
-    n_s = 24
+    n_s = ORACLE_SAMPLE_N
+    dt, desc = oracle_sample(args.physics, n_s, args.vf)
     scale = (args.res / n_s) ** 3          # oracle cost is linear in the node count
     return {"value": 1.0 / (dt * scale), "unit": "V-cycles/s", "cores": 1, "kind": "oracle",
             "sample": desc + f"; {dt:.2f} s, scaled by (N/{n_s})^3 = {scale:.0f} to the {args.res}^3 workload"}
@@ -175,12 +192,12 @@ def run_reference(args):
     if rank != 0:
         return
     steps = []
+    n_s = ORACLE_SAMPLE_N
     for _ in range(args.warmup):
-        oracle_sample(args.physics)
+        oracle_sample(args.physics, n_s, args.vf)
     for _ in range(args.steps):
-        dt, desc = oracle_sample(args.physics)
+        dt, desc = oracle_sample(args.physics, n_s, args.vf)
         steps.append(dt)
-    n_s = 24
     scale = (args.res / n_s) ** 3
     ms = float(np.mean(steps)) * scale * 1e3
     val = 1e3 / ms
@@ -341,6 +358,7 @@ def main():
     hbm, hbm_src = measured_peaks()
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     hbm_agg = hbm * world
+    traffic, traffic_src = ncu_traffic(args, world)
     value = 1e3 / ms
     dofs = dpn * nodes * nr
     out = {
@@ -356,7 +374,7 @@ def main():
         "dof_per_s": dofs * value,
         "roofline": {"bound": "hbm", "kernel": "level-0 damped-Jacobi sweep (k_fine_tiled + k_iface)",
                      "achieved": achieved, "peak": hbm_agg, "unit": "GB/s", "frac": achieved / hbm_agg,
-                     "traffic": None, "peak_source": hbm_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
                      "bytes_per_launch": bytes_launch, "bytes_rule": "148 B (elastic) x active nodes",
                      "active_nodes": n_act, "avg_launch_ms": avg_ms, "launches_timed": k_cnt,
                      "share_of_step": k_ms / args.steps / ms},
