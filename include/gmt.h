@@ -127,6 +127,24 @@ GMT_API int gmt_vcycle(gmt_problem p, int ncycles);
  * host arrays of NRHS doubles (abs_r / abs_f may be NULL).  Synchronises. */
 GMT_API int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f);
 
+/* Mixed-precision iterative refinement (single-device problems).  The level-0
+ * solution is fp32 and |u| grows like N in voxel units, so plain fp32 cycles
+ * stall at a relative residual of roughly N * 2^-24 (8e-5 at 512^3).  In
+ * refinement the solution is held as an unevaluated pair hi + lo of fp32
+ * arrays; each gmt_vcycle computes the defect f - K hi - K lo (difference-form
+ * kernels), runs one V-cycle on the fp32 correction from zero with the defect
+ * as right-hand side, and adds it with an error-free two-sum -- in exact
+ * arithmetic the same V-cycle.  mode: 0 = auto (default: gmt_solve switches
+ * when a cycle reduces the residual by less than 30 %), 1 = off (also leaves
+ * refinement, u = fp32(hi + lo)), 2 = on now.  gmt_get_solution returns
+ * fp32(hi + lo), gmt_homogenize evaluates C^H at hi (C^H is stationary at the
+ * solution), gmt_residual_norms the residual of hi + lo.  gmt_set_material /
+ * gmt_set_initial_guess leave refinement.  GMT_ERR_STATE for mode 2 on
+ * slab-partitioned problems. */
+GMT_API int gmt_set_refinement(gmt_problem p, int mode);
+/* 1 while the problem is in refinement, 0 otherwise. */
+GMT_API int gmt_refinement_active(gmt_problem p);
+
 /* Repeat V-cycles until max_m r_m <= rel_tol or max_cycles cycles ran.
  * *cycles_done / *final_rel (max over load cases) may be NULL; history, if
  * non-NULL, receives (max_cycles+1)*NRHS doubles: per-cycle residuals,

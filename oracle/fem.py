@@ -264,6 +264,21 @@ def loads_at_nodes(s: np.ndarray, phys: Physics, nodes) -> np.ndarray:
     return out
 
 
+def diagonal_at_nodes(s: np.ndarray, phys: Physics, nodes) -> np.ndarray:
+    """Sec. 4.6 Eq. 16 smoother diagonal D = diag(K) at the requested nodes:
+    sum over the 8 incident elements of s_e K_e[(k,c),(k,c)]; (len, dpn)."""
+    n = s.shape[0]
+    dpn = phys.dpn
+    out = np.zeros((len(nodes), dpn))
+    dK = np.diag(phys.Ke)
+    for t, (x, y, z) in enumerate(nodes):
+        for k in range(8):
+            kx, ky, kz = CORNERS[k]
+            se = float(s[(z - kz) % n, (y - ky) % n, (x - kx) % n])
+            out[t] += se * dK[k * dpn:(k + 1) * dpn]
+    return out
+
+
 def effective_tensor(s: np.ndarray, phys: Physics, u: np.ndarray) -> np.ndarray:
     """App. F1 / F2 "Effective Property Calculation":
         C^H_ij = 1/|Omega| sum_e (x_0^i - u_e^i)^T (s_e K_e) (x_0^j - u_e^j),

@@ -135,6 +135,13 @@ struct gmt_problem_s {
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
+  // mixed-precision iterative refinement (level 0): the solution is held as
+  // an unevaluated fp32 sum hi + lo; V-cycles run on the fp32 correction with
+  // the defect f - K (hi + lo) as explicit right-hand side
+  float *uhi = nullptr, *ulo = nullptr, *f0 = nullptr;
+  const float* f0_active = nullptr;   // explicit level-0 rhs during a refinement V-cycle
+  bool refine = false;
+  int refine_mode = 0;                // 0 auto (gmt_solve switches at the fp32 floor), 1 off, 2 always
   // kernel accounting and live profiling
   long long launches = 0;         // kernels executed (graph replays included)
   long long capture_count = 0;    // kernels recorded into the graph being captured
@@ -272,8 +279,10 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = b.cs;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
-    const bool packed = DPN == 3 && p->variant == 1, pairs = DPN == 3 && (p->variant == 2 || p->variant == 4);
-    const bool zb = p->variant == 3 || p->variant == 4;
+    // explicit right-hand side f (iterative refinement) only in the default kernels
+    const int var = f ? 0 : p->variant;
+    const bool packed = DPN == 3 && var == 1, pairs = DPN == 3 && (var == 2 || var == 4);
+    const bool zb = var == 3 || var == 4;
     const int NRG = DPN == 3 ? (packed || pairs ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
     const ZMap z = p->zm(0);
     const dim3 grid(p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
@@ -314,19 +323,28 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     } else {
       if (mode == M_JACOBI)
         k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                   cs, p->tflag, p->tntx, p->tnty);
+                                                                   cs, p->tflag, p->tntx, p->tnty, f);
       else
         k_fine_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                  cs, p->tflag, p->tntx, p->tnty);
+                                                                  cs, p->tflag, p->tntx, p->tnty, f);
     }
     LAUNCHED(p);
     if (nbi > 0) {
-      if (mode == M_JACOBI)
-        k_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
-                                                    p->icount);
-      else
-        k_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
-                                                   p->icount);
+      if (f) {
+        if (mode == M_JACOBI)
+          k_iface<DPN, M_JACOBI, true><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs,
+                                                            p->ilist, p->icount, f);
+        else
+          k_iface<DPN, M_RESID, true><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs,
+                                                           p->ilist, p->icount, f);
+      } else {
+        if (mode == M_JACOBI)
+          k_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
+                                                      p->icount);
+        else
+          k_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
+                                                     p->icount);
+      }
     } else {
       return GMT_OK;
     }
@@ -402,7 +420,7 @@ int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
 template <int DPN>
 int smooth(gmt_problem p, int l, int sweeps) {
   LevelBuf& b = p->lv[l];
-  const float* f = (l == 0) ? nullptr : b.f;
+  const float* f = (l == 0) ? p->f0_active : b.f;
   for (int it = 0; it < sweeps; ++it) {
     const float* src = (it & 1) ? b.t : b.u;
     float* dst = (it & 1) ? b.u : b.t;
@@ -433,7 +451,7 @@ int vcycle_once(gmt_problem p) {
     LevelBuf& b = p->lv[l];
     LevelBuf& c = p->lv[l + 1];
     TRY(smooth<DPN>(p, l, p->cfg.pre_sweeps));                                  // pre-smoothing
-    TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? nullptr : b.f, b.r, nullptr, 1));  // r = f - K u
+    TRY(launch_op<DPN>(p, l, M_RESID, b.u, l == 0 ? p->f0_active : b.f, b.r, nullptr, 1));  // r = f - K u
     TRY(launch_restrict<DPN>(p, l, b.r, c.f, true));                             // f^{l+1} = R r^l
     if (c.inj_pending) TRY(copy_in(p, c, c.u, c.inj, cudaMemcpyDeviceToDevice));
     else CK(cudaMemsetAsync(vbase(c, c.u), 0, vbytes(p, c), p->stream));        // u^{l+1} = 0 / e_hat
@@ -618,6 +636,16 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
   return GMT_OK;
 }
 
+// Number of fp64 partial rows the level-0 residual launch writes (tiled CTAs,
+// then interface blocks); fexp: explicit right-hand side (default kernels).
+template <int DPN>
+int l0_partials(gmt_problem p, bool fexp) {
+  const LevelBuf& b = p->lv[0];
+  const int v = fexp ? 0 : p->variant;
+  const int ng = DPN == 3 ? (v == 1 || v == 2 || v == 4 ? 3 : 2) : 1;
+  return p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * ng + (p->icount + 127) / 128;
+}
+
 template <int DPN>
 int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   constexpr int NR = Tr<DPN>::NR;
@@ -626,15 +654,75 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
   // of the tiled kernel followed by those of the interface kernel
   TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
-  TRY(reduce(p, p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * (DPN == 3 ? (p->variant == 1 || p->variant == 2 || p->variant == 4 ? 3 : 2) : 1) +
-                    (p->icount + 127) / 128,
-             2 * NR));
+  TRY(reduce(p, l0_partials<DPN>(p, false), 2 * NR));
   for (int m = 0; m < NR; ++m) {
     const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[NR + m]);
     if (rel) rel[m] = nf > 0 ? nr_ / nf : nr_;
     if (ar) ar[m] = nr_;
     if (af) af[m] = nf;
   }
+  return GMT_OK;
+}
+
+// ---- mixed-precision iterative refinement (level 0)
+
+int refine_alloc(gmt_problem p) {
+  LevelBuf& b = p->lv[0];
+  const ptrdiff_t goff = (ptrdiff_t)b.gh * b.n * b.n;
+  for (float** v : {&p->uhi, &p->ulo, &p->f0})
+    if (!*v) {
+      TRY(dalloc(p, (void**)v, vbytes(p, b)));
+      *v += goff;
+      CK(cudaMemsetAsync(vbase(b, *v), 0, vbytes(p, b), p->stream));
+    }
+  return GMT_OK;
+}
+
+// Start refinement from the current fp32 solution: hi = u, lo = 0.
+int refine_enter(gmt_problem p) {
+  TRY(refine_alloc(p));
+  LevelBuf& b = p->lv[0];
+  CK(cudaMemcpyAsync(vbase(b, p->uhi), vbase(b, b.u), vbytes(p, b), cudaMemcpyDeviceToDevice, p->stream));
+  CK(cudaMemsetAsync(vbase(b, p->ulo), 0, vbytes(p, b), p->stream));
+  p->refine = true;
+  return GMT_OK;
+}
+
+// Defect of the refined solution, f0 = (f - K hi) - K lo: both parts in the
+// difference form of the level-0 kernels (lo is tiny, its product is exact to
+// fp32).  With norms: pass 1 gives ||f||, pass 2 ||f - K (hi + lo)||.
+template <int DPN>
+int refine_defect(gmt_problem p, double* ar, double* af) {
+  constexpr int NR = Tr<DPN>::NR;
+  LevelBuf& b = p->lv[0];
+  const bool nrm = ar || af;
+  TRY(launch_op<DPN>(p, 0, M_RESID, p->uhi, nullptr, b.r, nrm ? p->part : nullptr, 1));
+  if (nrm) {
+    TRY(reduce(p, l0_partials<DPN>(p, false), 2 * NR));
+    for (int m = 0; m < NR; ++m) if (af) af[m] = std::sqrt(p->hred[NR + m]);
+  }
+  TRY(launch_op<DPN>(p, 0, M_RESID, p->ulo, b.r, p->f0, nrm ? p->part : nullptr, 1));
+  if (nrm) {
+    TRY(reduce(p, l0_partials<DPN>(p, true), 2 * NR));
+    for (int m = 0; m < NR; ++m) if (ar) ar[m] = std::sqrt(p->hred[m]);
+  }
+  return GMT_OK;
+}
+
+// One refinement cycle: defect, one V-cycle on the correction e (from 0)
+// with the defect as level-0 right-hand side, (hi, lo) += e.  In exact
+// arithmetic identical to one V-cycle on hi + lo.
+template <int DPN>
+int refine_cycle(gmt_problem p) {
+  LevelBuf& b = p->lv[0];
+  TRY(refine_defect<DPN>(p, nullptr, nullptr));
+  CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
+  p->f0_active = p->f0;
+  const int rc = vcycle_once<DPN>(p);
+  p->f0_active = nullptr;
+  TRY(rc);
+  k_refine_update<<<1184, 256, 0, p->stream>>>(p->code, p->uhi, p->ulo, b.u, (ptrdiff_t)b.nodes, p->V, b.cs);
+  LAUNCHED(p);
   return GMT_OK;
 }
 
@@ -678,6 +766,8 @@ void free_all(gmt_problem p) {
     if (b.tflag) cudaFree(b.tflag - (size_t)b.tntx * b.tnty * TF_GLO);
     cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.ilist);
   }
+  for (float* v : {p->uhi, p->ulo, p->f0})
+    if (v && !p->lv.empty()) cudaFree(vbase(p->lv[0], v));
   if (p->s) cudaFree(p->s - (size_t)p->N * p->N * MAT_GLO);
   cudaFree(p->M1g); cudaFree(p->M2g);
   if (p->tflag) cudaFree(p->tflag - (size_t)p->tntx * p->tnty * TF_GLO);
@@ -998,6 +1088,7 @@ int gmt_set_material(gmt_problem p, const void* material, int dtype, int locatio
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
   if (p->grp) return g_set_material(p->grp, material, dtype, location);
+  p->refine = false;
   TRY(upload_material(p, material, dtype, location));
   TRY(rebuild(p));
   return GMT_OK;
@@ -1007,6 +1098,7 @@ int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
   if (p->grp) return g_set_initial_guess(p->grp, u, location);
+  p->refine = false;
   LevelBuf& b = p->lv[0];
   if (!u) CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
   else TRY(copy_in(p, b, b.u, u, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
@@ -1018,6 +1110,7 @@ int gmt_inject_correction(gmt_problem p, int level, const float* e, int location
   if (level < 1) return fail(GMT_ERR_ARG, "injection level must be >= 1");
   TRY(no_group(p));
   TRY(set_device(p));
+  if (p->refine) return fail(GMT_ERR_STATE, "injection is not available during iterative refinement");
   LevelBuf& b = p->lv[level];
   if (!e) { b.inj_pending = false; return GMT_OK; }
   const size_t vb = b.nodes * p->V * sizeof(float);
@@ -1033,6 +1126,10 @@ int gmt_vcycle(gmt_problem p, int ncycles) {
   if (ncycles < 0) return fail(GMT_ERR_ARG, "ncycles < 0");
   TRY(set_device(p));
   if (p->grp) return g_vcycle(p->grp, ncycles);
+  if (p->refine) {
+    for (int c = 0; c < ncycles; ++c) TRY(p->dpn == 3 ? refine_cycle<3>(p) : refine_cycle<1>(p));
+    return GMT_OK;
+  }
   for (int c = 0; c < ncycles; ++c) {
     bool inj = false;
     for (auto& b : p->lv) inj |= b.inj_pending;
@@ -1114,6 +1211,16 @@ int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f)
   TRY(set_device(p));
   if (p->grp)
     return p->dpn == 3 ? g_residual_norms<3>(p->grp, rel, abs_r, abs_f) : g_residual_norms<1>(p->grp, rel, abs_r, abs_f);
+  if (p->refine) {
+    double ar[6], af[6];
+    TRY(p->dpn == 3 ? refine_defect<3>(p, ar, af) : refine_defect<1>(p, ar, af));
+    for (int m = 0; m < p->nr; ++m) {
+      if (rel) rel[m] = af[m] > 0 ? ar[m] / af[m] : ar[m];
+      if (abs_r) abs_r[m] = ar[m];
+      if (abs_f) abs_f[m] = af[m];
+    }
+    return GMT_OK;
+  }
   return p->dpn == 3 ? residual_norms<3>(p, rel, abs_r, abs_f) : residual_norms<1>(p, rel, abs_r, abs_f);
 }
 
@@ -1127,7 +1234,14 @@ int gmt_solve(gmt_problem p, double rel_tol, int max_cycles, int* cycles_done, d
   auto worst = [&]() { double w = 0; for (int m = 0; m < nr; ++m) w = std::max(w, rel[m]); return w; };
   if (history) for (int m = 0; m < nr; ++m) history[m] = rel[m];
   int k = 0;
+  if (!p->grp && p->refine_mode == 2 && !p->refine) TRY(refine_enter(p));
+  double prev = worst();
   while (k < max_cycles && worst() > rel_tol) {
+    // the fp32 solution stalls at a floor ~ N * 2^-24 relative residual
+    // (|u| grows like N in voxel units): switch to iterative refinement when
+    // a cycle no longer reduces the residual by 30 %
+    if (!p->grp && !p->refine && p->refine_mode == 0 && k >= 2 && worst() > 0.7 * prev) TRY(refine_enter(p));
+    prev = worst();
     TRY(gmt_vcycle(p, 1));
     ++k;
     TRY(gmt_residual_norms(p, rel, nullptr, nullptr));
@@ -1143,7 +1257,9 @@ int gmt_homogenize(gmt_problem p, double* CH) {
   if (!p || !CH) return fail(GMT_ERR_ARG, "null argument");
   TRY(set_device(p));
   if (p->grp) return p->dpn == 3 ? g_effective_tensor<3>(p->grp, CH) : g_effective_tensor<1>(p->grp, CH);
-  return p->dpn == 3 ? effective_tensor<3>(p, p->lv[0].u, CH) : effective_tensor<1>(p, p->lv[0].u, CH);
+  // refinement: C^H is stationary at the solution, so the fp32 part hi suffices
+  const float* u = p->refine ? p->uhi : p->lv[0].u;
+  return p->dpn == 3 ? effective_tensor<3>(p, u, CH) : effective_tensor<1>(p, u, CH);
 }
 
 int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) {
@@ -1154,7 +1270,7 @@ int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) 
   // user-layout working copy: the caller's device buffer, or the residual
   // buffer's storage (scratch between cycles, large enough for nodes * V)
   float* dst = (location == GMT_DEVICE) ? u : vbase(b, b.r);
-  TRY(copy_out(p, b, dst, b.u, cudaMemcpyDeviceToDevice));
+  TRY(copy_out(p, b, dst, p->refine ? p->uhi : b.u, cudaMemcpyDeviceToDevice));   // refinement: fp32(hi + lo) = hi
   k_mask_inactive<<<1184, 256, 0, p->stream>>>(p->code, dst, b.nodes, p->V);   // inactive nodes -> 0
   LAUNCHED(p);
   if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
@@ -1310,6 +1426,23 @@ int gmt_create_dist(const gmt_config* cfg, const void* material_slab, int materi
   if (!nccl_id) return fail(GMT_ERR_ARG, "nccl_id is NULL");
   return g_create(cfg, material_slab, material_dtype, material_location, nranks, rank, nccl_id, out);
 }
+
+int gmt_set_refinement(gmt_problem p, int mode) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (mode < 0 || mode > 2) return fail(GMT_ERR_ARG, "refinement mode must be 0 (auto), 1 (off) or 2 (on)");
+  if (p->grp && mode == 2) return fail(GMT_ERR_STATE, "iterative refinement is single-device only");
+  TRY(set_device(p));
+  p->refine_mode = mode;
+  if (mode == 2 && !p->refine) TRY(refine_enter(p));
+  if (mode == 1 && p->refine) {   // back to plain fp32 cycles on u = fp32(hi + lo)
+    LevelBuf& b = p->lv[0];
+    CK(cudaMemcpyAsync(vbase(b, b.u), vbase(b, p->uhi), vbytes(p, b), cudaMemcpyDeviceToDevice, p->stream));
+    p->refine = false;
+  }
+  return GMT_OK;
+}
+
+int gmt_refinement_active(gmt_problem p) { return p ? (p->refine ? 1 : 0) : GMT_ERR_ARG; }
 
 int gmt_num_slabs(gmt_problem p) { return !p ? GMT_ERR_ARG : (p->grp ? p->grp->P : 1); }
 

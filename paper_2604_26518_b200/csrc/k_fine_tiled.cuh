@@ -205,6 +205,11 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
           op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr,
                                       grp * NRG);
         } else {
+          if (f_all) {   // explicit right-hand side (iterative refinement: the defect)
+            const float* f = f_all + (ptrdiff_t)grp * V * cs;
+#pragma unroll
+            for (int k = 0; k < V; ++k) fl[k] = __ldg(f + k * cs + node);
+          }
           if constexpr (DPN == 3 && NRG == 2) node_uniform_pk(get, c, P.lam, P.mu, ui, acc, D);
           else node_uniform<DPN, NRG>(get, c, P.lam, P.mu, ui, acc, D);
           const float rc = __frcp_rn(c);
@@ -573,11 +578,13 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
 }
 
 // The general (interface) path over the static interface-node list.
-template <int DPN, int MODE>
+// FEXP: right-hand side read from fexp (iterative refinement) instead of the
+// element loads formed from the material.
+template <int DPN, int MODE, bool FEXP = false>
 __global__ void __launch_bounds__(128)
 k_iface(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap zu, float* __restrict__ out,
         int n, int nz, const FineConsts P, double* __restrict__ part, ptrdiff_t cs,
-        const int* __restrict__ list, int count) {
+        const int* __restrict__ list, int count, const float* __restrict__ fexp = nullptr) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "interface kernel: V-cycle modes only");
   using T = Tr<DPN>;
   constexpr int NR = T::NR, V = T::V;
@@ -604,7 +611,13 @@ k_iface(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, ZMap 
     float acc[V], fl[V], ui[V], D[DPN];
 #pragma unroll
     for (int k = 0; k < V; ++k) ui[k] = __ldg(u + k * cs + node);
-    node_general<DPN, true, true>(get, sc, P.lam, P.mu, ui, acc, fl, D);
+    if constexpr (FEXP) {
+      node_general<DPN, false, true>(get, sc, P.lam, P.mu, ui, acc, fl, D);
+#pragma unroll
+      for (int k = 0; k < V; ++k) fl[k] = __ldg(fexp + k * cs + node);
+    } else {
+      node_general<DPN, true, true>(get, sc, P.lam, P.mu, ui, acc, fl, D);
+    }
     op_epilogue<DPN, MODE>(true, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr);
   }
   if (part) block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)blockIdx.x * 2 * NR);

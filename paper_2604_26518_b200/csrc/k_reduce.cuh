@@ -179,6 +179,31 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
   block_reduce_store<NQ>(q, part + (ptrdiff_t)blockIdx.x * NQ);
 }
 
+// Iterative refinement: (hi, lo) += e on active level-0 nodes (code != 0;
+// e is zero elsewhere).  Error-free two-sum of hi + e, the rounding error
+// folded into lo, then a fast renormalisation so |lo| <= ulp(hi) / 2: the
+// pair carries ~48 significant bits, enough that the fp32 rounding of the
+// solution no longer limits the attainable residual.
+__global__ void __launch_bounds__(256)
+k_refine_update(const float* __restrict__ code, float* __restrict__ hi, float* __restrict__ lo,
+                const float* __restrict__ e, ptrdiff_t nodes, int V, ptrdiff_t cs) {
+  for (ptrdiff_t i = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; i < nodes;
+       i += (ptrdiff_t)gridDim.x * blockDim.x) {
+    if (__ldg(code + i) == 0.f) continue;
+    for (int k = 0; k < V; ++k) {
+      const ptrdiff_t j = k * cs + i;
+      const float a = hi[j], b = e[j];
+      const float sm = __fadd_rn(a, b);
+      const float bb = __fsub_rn(sm, a);
+      const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(sm, bb)), __fsub_rn(b, bb));
+      const float l = __fadd_rn(lo[j], err);
+      const float h = __fadd_rn(sm, l);
+      lo[j] = __fsub_rn(l, __fsub_rn(h, sm));
+      hi[j] = h;
+    }
+  }
+}
+
 // Sum of u over active nodes per (m, c) and the active-node count (level 0).
 template <int DPN>
 __global__ void __launch_bounds__(128)

@@ -81,6 +81,8 @@ SIGNATURES = {
     "gmt_create_dist": (C.c_int, [C.POINTER(gmt_config), C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_void_p, C.POINTER(C.c_void_p)]),
     "gmt_num_slabs": (C.c_int, [_P]),
+    "gmt_set_refinement": (C.c_int, [_P, C.c_int]),
+    "gmt_refinement_active": (C.c_int, [_P]),
 }
 
 _lib = None
@@ -289,6 +291,13 @@ class Problem:
         ptr, loc = _buf(out, np.float32)
         _check(self.lib.gmt_get_solution(self._h, ptr, loc, int(zero_mean)), "gmt_get_solution")
         return out
+
+    def gmt_set_refinement(self, mode: int):
+        """0 auto (default), 1 off, 2 on: mixed-precision iterative refinement."""
+        _check(self.lib.gmt_set_refinement(self._h, int(mode)), "gmt_set_refinement")
+
+    def gmt_refinement_active(self) -> bool:
+        return bool(self.lib.gmt_refinement_active(self._h))
 
     def gmt_sync(self):
         _check(self.lib.gmt_sync(self._h), "gmt_sync")

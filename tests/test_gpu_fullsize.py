@@ -1,0 +1,108 @@
+"""Parity at BASELINE.json's full size: the 512^3 elasticity gyroid (v_f 0.3,
+6 load cases) that bench.py times, in the launch configuration it times.
+
+* One level-0 damped-Jacobi sweep through the tiled + interface kernels
+  (levels = 1, one coarsest sweep: gmt_vcycle is then exactly that sweep) is
+  compared node by node with the FP64 oracle on ~300 sampled nodes: tile and
+  z-chunk boundaries, the periodic seams, interface, interior and void nodes
+  (oracle: apply_K_at_nodes / loads_at_nodes / diagonal_at_nodes, Sec. 4.6
+  Eq. 14-16).  Tolerance 1e-5 of the sample's largest update.
+* A full GMG solve of the 8-level hierarchy to 1e-5 relative residual
+  (north star) is checked through properties that hold at any size: monotone
+  residual decrease, C^H symmetric positive definite, below the Voigt bound
+  v_f C_0 (App. F1 energy minimum <= the u = 0 energy), and the cubic symmetry
+  of the gyroid (C11 = C22 = C33, C44 = C55 = C66, no normal/shear coupling).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import fem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+N = 512
+OMEGA = 0.45
+
+
+@pytest.fixture(scope="module")
+def workload():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_26518_b200 import build
+    build.build()
+    s = synth.tpms(N, "gyroid", 0.3)
+    return s
+
+
+def _sample_nodes(s, rng):
+    n = s.shape[0]
+    occ = s > 0
+    nodes = set()
+    edges = [0, 1, 3, 4, 15, 16, 17, 31, 32, 33, 255, 256, n - 2, n - 1]
+    for x in edges:
+        for y in (0, 3, 4, n - 1):
+            for z in (0, 15, 16, n - 1):
+                if rng.random() < 0.35:
+                    nodes.add((x, y, z))
+    # classify random nodes by their 8 incident voxels
+    want = {"interface": 80, "interior": 60, "void": 20}
+    got = {k: 0 for k in want}
+    while any(got[k] < want[k] for k in want):
+        x, y, z = (int(v) for v in rng.integers(0, n, 3))
+        vox = [occ[(z - kz) % n, (y - ky) % n, (x - kx) % n] for kx, ky, kz in fem.CORNERS]
+        kind = "interior" if all(vox) else ("void" if not any(vox) else "interface")
+        if got[kind] < want[kind]:
+            got[kind] += 1
+            nodes.add((x, y, z))
+    return sorted(nodes)
+
+
+def test_one_tiled_jacobi_sweep_sampled(workload):
+    from paper_2604_26518_b200 import Problem
+    s = workload
+    u0 = synth.initial_guess(N, 6, 3, seed=1, material=s)          # [m, c, z, y, x]
+    with Problem(s, physics="elastic", levels=1, coarse_sweeps=1, omega=OMEGA) as P:
+        assert P.levels == 1
+        P.gmt_set_initial_guess(u0)
+        P.gmt_vcycle(1)
+        u1 = P.gmt_get_solution()
+    ph = fem.Physics("elastic")
+    rng = np.random.default_rng(11)
+    nodes = _sample_nodes(s, rng)
+    Ku = fem.apply_K_at_nodes(s, ph, lambda x, y, z: u0[:, :, z, y, x], nodes)   # (len, M, dpn)
+    f = fem.loads_at_nodes(s, ph, nodes)
+    D = fem.diagonal_at_nodes(s, ph, nodes)                                        # (len, dpn)
+    want = np.zeros((len(nodes), 6, 3))
+    got = np.zeros_like(want)
+    for t, (x, y, z) in enumerate(nodes):
+        if D[t].max() > 0:   # active node: u + omega D^-1 (f - K u); inactive nodes are returned as 0
+            want[t] = u0[:, :, z, y, x] + OMEGA * (f[t] - Ku[t]) / D[t][None, :]
+        got[t] = u1[:, :, z, y, x]
+    err = np.abs(got - want)
+    assert err.max() <= 1e-5 * np.abs(want).max(), (err.max(), np.abs(want).max())
+    n_iface = sum(1 for t in range(len(nodes)) if 0 < D[t].max() and not np.allclose(f[t], 0))
+    assert n_iface >= 40
+
+
+def test_full_solve_tensor_properties(workload):
+    from paper_2604_26518_b200 import Problem
+    s = workload
+    vf = float(s.mean())
+    with Problem(s, physics="elastic", omega=OMEGA) as P:
+        assert P.levels == 8
+        k, fr, hist = P.gmt_solve(1e-5, 80)
+        CH = P.gmt_homogenize()
+    assert fr <= 1e-5, (k, fr)
+    worst = hist.max(axis=1)
+    assert np.all(np.diff(worst) < 0), worst
+    ph = fem.Physics("elastic")
+    assert np.abs(CH - CH.T).max() <= 1e-12 * np.abs(CH).max()
+    ev = np.linalg.eigvalsh(0.5 * (CH + CH.T))
+    assert ev.min() > 0
+    assert np.linalg.eigvalsh(vf * ph.C0 - CH).min() >= -1e-6 * np.abs(CH).max()   # Voigt bound
+    d = np.diag(CH)
+    assert np.ptp(d[:3]) <= 1e-4 * d[0] and np.ptp(d[3:]) <= 1e-4 * d[3]
+    assert np.abs(CH[:3, 3:]).max() <= 1e-4 * d[0]
+    assert abs(CH[0, 1] - CH[0, 2]) <= 1e-4 * d[0] and abs(CH[0, 1] - CH[1, 2]) <= 1e-4 * d[0]

@@ -184,6 +184,20 @@ def test_loads(kind):
         assert np.abs(fs[t] - f[z, y, x]).max() < 1e-14
 
 
+@pytest.mark.parametrize("kind", ["elastic", "thermal"])
+def test_diagonal_at_nodes_matches_assembled(kind):
+    """diagonal_at_nodes (per-node element loop) == diag of the assembled K."""
+    ph = fem.Physics(kind)
+    n = 5
+    s = synth.random_density(n, 0.0, 1.0, seed=7)
+    s[s < 0.4] = 0.0
+    d = fem.to_node_layout(fem.assemble_K(s, ph).diagonal()[:, None], n, ph.dpn)   # (z, y, x, 1, dpn)
+    nodes = [(0, 0, 0), (4, 1, 3), (2, 2, 2), (1, 4, 0)]
+    got = fem.diagonal_at_nodes(s, ph, nodes)
+    for t, (x, y, z) in enumerate(nodes):
+        assert np.abs(got[t] - d[z, y, x, 0]).max() < 1e-13
+
+
 def test_effective_tensor_solid_is_base_tensor():
     for kind in ("elastic", "thermal"):
         ph = fem.Physics(kind, E=1.3, nu=0.25, kappa=0.8)
