@@ -616,7 +616,7 @@ template <int DPN>
 int effective_tensor(gmt_problem p, const float* u, double* CH) {
   constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
   const LevelBuf& b = p->lv[0];
-  const int nblk = std::max(1, std::min((p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
+  const int nblk = std::max(1, std::min((2 * p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
   {
     Prof prof(p, 7);
     k_effective_tensor<DPN><<<nblk, CH_THREADS, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,

@@ -69,7 +69,12 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
   double q[NQ];
 #pragma unroll
   for (int k = 0; k < NQ; ++k) q[k] = 0.0;
-  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < ecount; it += gridDim.x * blockDim.x) {
+  // work item = (element, z-half): adjacent lanes take the two halves of one
+  // element, so each corner gather serves both from the same sectors
+  const long long items = 2ll * ecount;
+  for (long long ii = blockIdx.x * (long long)blockDim.x + threadIdx.x; ii < items;
+       ii += (long long)gridDim.x * blockDim.x) {
+    const int it = (int)(ii >> 1), h = (int)(ii & 1);
     const ptrdiff_t eid = __ldg(elist + it);
     const float se = __ldg(s + eid);
     const int x = (int)(eid % n), y = (int)((eid / n) % n), z = (int)(eid / plane);
@@ -81,8 +86,7 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
     f2 qf[NQ];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) qf[k] = 0ull;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
+    {
       const float gz = h ? G1 : G0;
 #pragma unroll 3
       for (int m = 0; m < NR; ++m) {
