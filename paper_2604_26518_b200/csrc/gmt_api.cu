@@ -280,13 +280,15 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   const ptrdiff_t cs = b.cs;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
     // explicit right-hand side f (iterative refinement) only in the default kernels
-    const int var = f ? 0 : p->variant;
+    int var = f ? 0 : p->variant;
+    if (p->variant == 5) var = b.n % TX_X == 0 ? 5 : 0;   // x-pairs (n % 64 == 0) also take an explicit rhs
     const bool packed = DPN == 3 && var == 1, pairs = DPN == 3 && (var == 2 || var == 4);
-    const bool zb = var == 3 || var == 4;
+    const bool zb = var == 3 || var == 4, x2 = var == 5;
     const int NRG = DPN == 3 ? (packed || pairs ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
     const ZMap z = p->zm(0);
-    const dim3 grid(p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
-    const size_t shm = (size_t)(zb ? TT_NB2 : TT_NB) * NRG * DPN * TT_PLS * sizeof(float);
+    const dim3 grid(x2 ? b.n / TX_X : p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
+    const size_t shm = x2 ? (size_t)TT_NB * NRG * DPN * TX_PLS * sizeof(float)
+                          : (size_t)(zb ? TT_NB2 : TT_NB) * NRG * DPN * TT_PLS * sizeof(float);
     const int nbt = grid.x * grid.y * grid.z;
     double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
     const int nbi = (p->icount + 127) / 128;
@@ -297,6 +299,13 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
       else
         k_fine_tiled2<M_RESID><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
                                                          p->tntx, p->tnty);
+    } else if (x2) {
+      if (mode == M_JACOBI)
+        k_fine_tiled_x2<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                    cs, p->tflag, p->tntx, p->tnty, f);
+      else
+        k_fine_tiled_x2<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                   cs, p->tflag, p->tntx, p->tnty, f);
     } else if (zb) {
       if (pairs) {
         if (mode == M_JACOBI)
@@ -321,12 +330,21 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
         k_fine_tiled<3, M_RESID, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
                                                               p->tflag, p->tntx, p->tnty);
     } else {
-      if (mode == M_JACOBI)
-        k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                   cs, p->tflag, p->tntx, p->tnty, f);
-      else
-        k_fine_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                  cs, p->tflag, p->tntx, p->tnty, f);
+      if (f) {
+        if (mode == M_JACOBI)
+          k_fine_tiled<DPN, M_JACOBI, 3, false, true><<<grid, block, shm, st>>>(
+              p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag, p->tntx, p->tnty, f);
+        else
+          k_fine_tiled<DPN, M_RESID, 3, false, true><<<grid, block, shm, st>>>(
+              p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag, p->tntx, p->tnty, f);
+      } else {
+        if (mode == M_JACOBI)
+          k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                     cs, p->tflag, p->tntx, p->tnty);
+        else
+          k_fine_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
+                                                                    cs, p->tflag, p->tntx, p->tnty);
+      }
     }
     LAUNCHED(p);
     if (nbi > 0) {
@@ -641,9 +659,11 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
 template <int DPN>
 int l0_partials(gmt_problem p, bool fexp) {
   const LevelBuf& b = p->lv[0];
-  const int v = fexp ? 0 : p->variant;
+  int v = fexp ? 0 : p->variant;
+  if (p->variant == 5) v = b.n % TX_X == 0 ? 5 : 0;
   const int ng = DPN == 3 ? (v == 1 || v == 2 || v == 4 ? 3 : 2) : 1;
-  return p->tntx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * ng + (p->icount + 127) / 128;
+  const int gx = v == 5 ? b.n / TX_X : p->tntx;
+  return gx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * ng + (p->icount + 127) / 128;
 }
 
 template <int DPN>
@@ -999,6 +1019,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     const int shm1 = TT_NB * 3 * TT_PLS * (int)sizeof(float);
     const int shm3z = TT_NB2 * 9 * TT_PLS * (int)sizeof(float), shm2z = TT_NB2 * 6 * TT_PLS * (int)sizeof(float);
     const int shm1z = TT_NB2 * 3 * TT_PLS * (int)sizeof(float);
+    const int shm3x = TT_NB * 9 * TX_PLS * (int)sizeof(float), shm1x = TT_NB * 3 * TX_PLS * (int)sizeof(float);
     if (cudaFuncSetAttribute(k_fine_tiled2<M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled2<M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
@@ -1007,6 +1028,10 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3z) ||
@@ -1014,7 +1039,11 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
         cudaFuncSetAttribute(k_fine_tiled_zb<3, M_RESID, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
         cudaFuncSetAttribute(k_fine_tiled_zb<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z))
+        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z) ||
+        cudaFuncSetAttribute(k_fine_tiled_x2<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3x) ||
+        cudaFuncSetAttribute(k_fine_tiled_x2<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3x) ||
+        cudaFuncSetAttribute(k_fine_tiled_x2<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1x) ||
+        cudaFuncSetAttribute(k_fine_tiled_x2<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1x))
       return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
   }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);

@@ -60,10 +60,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef TT_MINB
 #define TT_MINB 5
 #endif
+#ifndef TX_MINB
+#define TX_MINB 3
+#endif
 #ifndef TT_MINB2
 #define TT_MINB2 3
 #endif
-template <int DPN, int MODE, int NRG, bool COARSE = false>
+template <int DPN, int MODE, int NRG, bool COARSE = false, bool FEXP = false>
 __global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB)
 k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
              float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
@@ -205,7 +208,7 @@ k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ 
           op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acc, fl, ui, D, P.omega, nrm, part != nullptr,
                                       grp * NRG);
         } else {
-          if (f_all) {   // explicit right-hand side (iterative refinement: the defect)
+          if constexpr (FEXP) {   // explicit right-hand side (iterative refinement: the defect)
             const float* f = f_all + (ptrdiff_t)grp * V * cs;
 #pragma unroll
             for (int k = 0; k < V; ++k) fl[k] = __ldg(f + k * cs + node);
@@ -373,6 +376,194 @@ k_fine_tiled_zb(const float* __restrict__ code, ZMap zs, const float* __restrict
       if (u1)
         op_epilogue<DPN, MODE, NRG>(valid, out + node + plane, cs, acc1, fl, ui1, D1, P.omega, nrm,
                                     part != nullptr, grp * NRG, Dinv1);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if ((MODE == M_RESID || MODE == M_JACOBI) && part) {
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_reduce_store<2 * NR>(nrm, part + (ptrdiff_t)b * 2 * NR);
+  }
+}
+
+// Level-0 sweep with two x-adjacent nodes per thread ("x-pairs"): a CTA of
+// 32 x 4 threads owns a 64 x 4 column of nodes.  For every (dy, dz) row and
+// component the thread reads the 4 values x-1 .. x+2 -- one LDS.64 for the
+// aligned pair (x, x+1) plus two LDS.32 -- instead of 3 loads per node, which
+// cuts the shared-memory instructions per node in half and the wavefronts by
+// a third; the 64-wide tiles also halve the halo columns per node.  Same
+// arithmetic as node_uniform (difference form, H(d) = H(-d) pairing).
+constexpr int TX_X = 64, TX_RS = 72, TX_PLS = TT_PY * TX_RS;   // interior at 4 .. 67, halos at 3 and 68
+template <int DPN, int NRG>
+__device__ __forceinline__ void uniform_pair(const float* __restrict__ sl0, const float* __restrict__ sl1,
+                                             const float* __restrict__ sl2, int base, float lam, float mu,
+                                             const float (&ua)[NRG * DPN], const float (&ub)[NRG * DPN],
+                                             float (&acca)[NRG * DPN], float (&accb)[NRG * DPN]) {
+  constexpr int V = NRG * DPN;
+  const float* sl[3] = {sl0, sl1, sl2};
+#pragma unroll
+  for (int k = 0; k < V; ++k) acca[k] = accb[k] = 0.f;
+#pragma unroll
+  for (int d = 14; d < 27; ++d) {   // d and 26-d are opposite offsets
+    const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+    float wa[V], wb[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      // row (dy, dz) and the opposite row (-dy, -dz): values at x-1 .. x+2
+      const float* ra = sl[dz + 1] + k * TX_PLS + base + dy * TX_RS;
+      const float* rb = sl[1 - dz] + k * TX_PLS + base - dy * TX_RS;
+      const float2 pa = *reinterpret_cast<const float2*>(ra), pb = *reinterpret_cast<const float2*>(rb);
+      const float a_m = ra[-1], a_p = ra[2], b_m = rb[-1], b_p = rb[2];
+      // node A (x): +d -> row a at x+dx, -d -> row b at x-dx; node B (x+1) likewise
+      const float aA = dx < 0 ? a_m : (dx > 0 ? pa.y : pa.x), bA = dx > 0 ? b_m : (dx < 0 ? pb.y : pb.x);
+      const float aB = dx < 0 ? pa.x : (dx > 0 ? a_p : pa.y), bB = dx > 0 ? pb.x : (dx < 0 ? b_p : pb.y);
+      wa[k] = (aA - ua[k]) + (bA - ua[k]);
+      wb[k] = (aB - ub[k]) + (bB - ub[k]);
+    }
+#pragma unroll
+    for (int p = 0; p < DPN; ++p)
+#pragma unroll
+      for (int q = 0; q < DPN; ++q) {
+        if (!hom_nz(d, p, q)) continue;
+        const int i = d * DPN * DPN + p * DPN + q;
+        const float h = CT<DPN>::two ? fmaf(lam, CT<DPN>::Hl(i), mu * CT<DPN>::Hm(i)) : lam * CT<DPN>::Hl(i);
+#pragma unroll
+        for (int m = 0; m < NRG; ++m) {
+          acca[m * DPN + p] = fmaf(h, wa[m * DPN + q], acca[m * DPN + p]);
+          accb[m * DPN + p] = fmaf(h, wb[m * DPN + q], accb[m * DPN + p]);
+        }
+      }
+  }
+}
+
+template <int DPN, int MODE, int NRG>
+__global__ void __launch_bounds__(TT_X * TT_Y, TX_MINB)
+k_fine_tiled_x2(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
+                float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
+                ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty,
+                const float* __restrict__ f_all = nullptr) {
+  static_assert(MODE == M_JACOBI || MODE == M_RESID, "tiled kernel: V-cycle modes only");
+  using T = Tr<DPN>;
+  constexpr int NR = T::NR, V = NRG * DPN, NG = NR / NRG;
+  const int grp = blockIdx.z % NG, chunk = blockIdx.z / NG;
+  const float* __restrict__ u = u_all + (ptrdiff_t)grp * V * cs;
+  float* __restrict__ out = out_all + (ptrdiff_t)grp * V * cs;
+  constexpr int NTH = TT_X * TT_Y;
+  extern __shared__ __align__(16) float smem[];   // [TT_NB][V][TT_PY][TX_RS]
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * TT_X + tx;
+  const int x0 = blockIdx.x * TX_X, y0 = blockIdx.y * TT_Y;   // requires n % 64 == 0
+  const int z0 = chunk * TT_ZC, z1 = min(nz, z0 + TT_ZC);
+  const int xa = x0 + 2 * tx, y = y0 + ty;
+  const bool valid = y < n;
+  const int yc = valid ? y : 0;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+
+  // tile flags: this CTA covers the 32-wide flag tiles 2 bx and 2 bx + 1
+  const int lane = tid & 31;
+  bool fl_on = false;
+  if (lane < TT_ZC + 5) {
+    const uint8_t* fr = flag + ((ptrdiff_t)zs(z0 - 3 + lane) * nty + blockIdx.y) * ntx + 2 * blockIdx.x;
+    fl_on = (fr[0] | fr[1]) != 0;
+  }
+  const unsigned fm = __ballot_sync(0xffffffffu, fl_on);
+  auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1u; };
+  auto needed = [&](int p) -> bool { return (fm >> (p - z0 + 1)) & 0xfu; };
+  // staging: per (component, row) 16 x 16-byte interior chunks + 2 halo floats
+  constexpr int NCH = V * TT_PY * 16, NHA = V * TT_PY * 2;
+  constexpr int CPT = (NCH + NTH - 1) / NTH;
+  static_assert(NHA <= NTH, "one halo float per thread");
+  ptrdiff_t c_src[CPT];
+  int c_dst[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int q = tid + i * NTH;
+    const int k = q / (TT_PY * 16), rem = q - k * (TT_PY * 16);
+    const int py = rem / 16, c = rem - py * 16;
+    c_src[i] = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + x0 + 4 * c;
+    c_dst[i] = q < NCH ? k * TX_PLS + py * TX_RS + 4 + 4 * c : -1;
+  }
+  ptrdiff_t h_src = 0;
+  int h_dst = -1;
+  if (tid < NHA) {
+    const int k = tid / (TT_PY * 2), rem = tid - k * (TT_PY * 2);
+    const int py = rem >> 1, side = rem & 1;
+    h_src = (ptrdiff_t)k * cs + (ptrdiff_t)wrapi(y0 - 1 + py, n) * n + wrapi(side ? x0 + TX_X : x0 - 1, n);
+    h_dst = k * TX_PLS + py * TX_RS + (side ? 4 + TX_X : 3);
+  }
+  auto slot = [&](int p) -> float* { return smem + (size_t)((p + 2 * TT_NB) % TT_NB) * V * TX_PLS; };
+  auto issue = [&](int p) {
+    float* dst = slot(p);
+    const float* src = u + (ptrdiff_t)zu(p) * plane;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+      if (c_dst[i] >= 0) cp_async16(dst + c_dst[i], src + c_src[i]);
+    if (h_dst >= 0) cp_async4(dst + h_dst, src + h_src);
+  };
+
+  double nrm[2 * NR];
+#pragma unroll
+  for (int k = 0; k < 2 * NR; ++k) nrm[k] = 0.0;
+  for (int p = z0 - 1; p <= z0 + TT_AHEAD - 1; ++p) {
+    if (p <= z1 && needed(p)) issue(p);
+    cp_async_commit();
+  }
+  const float* code_col = code + (ptrdiff_t)yc * n + xa;
+  float2 c_next = valid ? *reinterpret_cast<const float2*>(code_col + (ptrdiff_t)z0 * plane) : make_float2(0.f, 0.f);
+  const int base = (ty + 1) * TX_RS + 4 + 2 * tx;
+  for (int z = z0; z < z1; ++z) {
+    const float2 cc = c_next;
+    if (z + 1 < z1)
+      c_next = valid ? *reinterpret_cast<const float2*>(code_col + (ptrdiff_t)(z + 1) * plane) : make_float2(0.f, 0.f);
+    if (z + TT_AHEAD <= z1 && needed(z + TT_AHEAD)) issue(z + TT_AHEAD);
+    cp_async_commit();
+    cp_async_wait<TT_AHEAD - 1>();
+    __syncthreads();
+    const bool ua_ = cc.x > 0.f, ub_ = cc.y > 0.f;
+    if ((vflag(z - 1) || vflag(z)) && (ua_ || ub_)) {
+      const float* s0 = slot(z - 1);
+      const float* s1 = slot(z);
+      const float* s2 = slot(z + 1);
+      float uia[V], uib[V], acca[V], accb[V], fla[V], flb[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float2 c2 = *reinterpret_cast<const float2*>(s1 + k * TX_PLS + base);
+        uia[k] = c2.x;
+        uib[k] = c2.y;
+        fla[k] = flb[k] = 0.f;
+      }
+      const ptrdiff_t node = (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xa;
+      if (f_all) {
+        const float* f = f_all + (ptrdiff_t)grp * V * cs;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const float2 f2v = *reinterpret_cast<const float2*>(f + k * cs + node);
+          fla[k] = f2v.x;
+          flb[k] = f2v.y;
+        }
+      }
+      uniform_pair<DPN, NRG>(s0, s1, s2, base, P.lam, P.mu, uia, uib, acca, accb);
+      const float ca = ua_ ? cc.x : 1.f, cb = ub_ ? cc.y : 1.f;
+      float Da[DPN], Db[DPN], Dia[DPN], Dib[DPN];
+      const float ra = __frcp_rn(ca), rb = __frcp_rn(cb);
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) {
+        Da[p] = Db[p] = 0.f;
+        Dia[p] = P.wd[p] * ra;
+        Dib[p] = P.wd[p] * rb;
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        acca[k] *= ca;
+        accb[k] *= cb;
+      }
+      if (ua_)
+        op_epilogue<DPN, MODE, NRG>(valid, out + node, cs, acca, fla, uia, Da, P.omega, nrm, part != nullptr,
+                                    grp * NRG, Dia);
+      if (ub_)
+        op_epilogue<DPN, MODE, NRG>(valid, out + node + 1, cs, accb, flb, uib, Db, P.omega, nrm, part != nullptr,
+                                    grp * NRG, Dib);
     }
     __syncthreads();
   }
