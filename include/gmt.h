@@ -127,7 +127,7 @@ GMT_API int gmt_vcycle(gmt_problem p, int ncycles);
  * host arrays of NRHS doubles (abs_r / abs_f may be NULL).  Synchronises. */
 GMT_API int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f);
 
-/* Mixed-precision iterative refinement (single-device problems).  The level-0
+/* Mixed-precision iterative refinement.  The level-0
  * solution is fp32 and |u| grows like N in voxel units, so plain fp32 cycles
  * stall at a relative residual of roughly N * 2^-24 (8e-5 at 512^3).  In
  * refinement the solution is held as an unevaluated pair hi + lo of fp32
@@ -139,8 +139,8 @@ GMT_API int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double
  * refinement, u = fp32(hi + lo)), 2 = on now.  gmt_get_solution returns
  * fp32(hi + lo), gmt_homogenize evaluates C^H at hi (C^H is stationary at the
  * solution), gmt_residual_norms the residual of hi + lo.  gmt_set_material /
- * gmt_set_initial_guess leave refinement.  GMT_ERR_STATE for mode 2 on
- * slab-partitioned problems. */
+ * gmt_set_initial_guess leave refinement.  Slab-partitioned problems refine
+ * the same way (the hi / lo ghost planes are exchanged for the defect). */
 GMT_API int gmt_set_refinement(gmt_problem p, int mode);
 /* 1 while the problem is in refinement, 0 otherwise. */
 GMT_API int gmt_refinement_active(gmt_problem p);

@@ -1154,6 +1154,10 @@ int gmt_vcycle(gmt_problem p, int ncycles) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   if (ncycles < 0) return fail(GMT_ERR_ARG, "ncycles < 0");
   TRY(set_device(p));
+  if (p->grp && p->refine) {
+    for (int c = 0; c < ncycles; ++c) TRY(p->dpn == 3 ? g_refine_cycle<3>(p->grp) : g_refine_cycle<1>(p->grp));
+    return GMT_OK;
+  }
   if (p->grp) return g_vcycle(p->grp, ncycles);
   if (p->refine) {
     for (int c = 0; c < ncycles; ++c) TRY(p->dpn == 3 ? refine_cycle<3>(p) : refine_cycle<1>(p));
@@ -1238,11 +1242,12 @@ long long gmt_kernel_launches(gmt_problem p) {
 int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double* abs_f) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   TRY(set_device(p));
-  if (p->grp)
+  if (p->grp && !p->refine)
     return p->dpn == 3 ? g_residual_norms<3>(p->grp, rel, abs_r, abs_f) : g_residual_norms<1>(p->grp, rel, abs_r, abs_f);
   if (p->refine) {
     double ar[6], af[6];
-    TRY(p->dpn == 3 ? refine_defect<3>(p, ar, af) : refine_defect<1>(p, ar, af));
+    if (p->grp) TRY(p->dpn == 3 ? g_refine_defect<3>(p->grp, ar, af) : g_refine_defect<1>(p->grp, ar, af));
+    else TRY(p->dpn == 3 ? refine_defect<3>(p, ar, af) : refine_defect<1>(p, ar, af));
     for (int m = 0; m < p->nr; ++m) {
       if (rel) rel[m] = af[m] > 0 ? ar[m] / af[m] : ar[m];
       if (abs_r) abs_r[m] = ar[m];
@@ -1263,13 +1268,14 @@ int gmt_solve(gmt_problem p, double rel_tol, int max_cycles, int* cycles_done, d
   auto worst = [&]() { double w = 0; for (int m = 0; m < nr; ++m) w = std::max(w, rel[m]); return w; };
   if (history) for (int m = 0; m < nr; ++m) history[m] = rel[m];
   int k = 0;
-  if (!p->grp && p->refine_mode == 2 && !p->refine) TRY(refine_enter(p));
+  auto enter = [&]() { return p->grp ? g_refine_enter(p->grp) : refine_enter(p); };
+  if (p->refine_mode == 2 && !p->refine) TRY(enter());
   double prev = worst();
   while (k < max_cycles && worst() > rel_tol) {
     // the fp32 solution stalls at a floor ~ N * 2^-24 relative residual
     // (|u| grows like N in voxel units): switch to iterative refinement when
     // a cycle no longer reduces the residual by 30 %
-    if (!p->grp && !p->refine && p->refine_mode == 0 && k >= 2 && worst() > 0.7 * prev) TRY(refine_enter(p));
+    if (!p->refine && p->refine_mode == 0 && k >= 2 && worst() > 0.7 * prev) TRY(enter());
     prev = worst();
     TRY(gmt_vcycle(p, 1));
     ++k;
@@ -1459,14 +1465,16 @@ int gmt_create_dist(const gmt_config* cfg, const void* material_slab, int materi
 int gmt_set_refinement(gmt_problem p, int mode) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
   if (mode < 0 || mode > 2) return fail(GMT_ERR_ARG, "refinement mode must be 0 (auto), 1 (off) or 2 (on)");
-  if (p->grp && mode == 2) return fail(GMT_ERR_STATE, "iterative refinement is single-device only");
   TRY(set_device(p));
-  p->refine_mode = mode;
-  if (mode == 2 && !p->refine) TRY(refine_enter(p));
+  std::vector<gmt_problem> parts = p->grp ? p->grp->slabs : std::vector<gmt_problem>{p};
+  for (auto q : parts) q->refine_mode = mode;
+  if (mode == 2 && !p->refine) TRY(p->grp ? g_refine_enter(p->grp) : refine_enter(p));
   if (mode == 1 && p->refine) {   // back to plain fp32 cycles on u = fp32(hi + lo)
-    LevelBuf& b = p->lv[0];
-    CK(cudaMemcpyAsync(vbase(b, b.u), vbase(b, p->uhi), vbytes(p, b), cudaMemcpyDeviceToDevice, p->stream));
-    p->refine = false;
+    for (auto q : parts) {
+      LevelBuf& b = q->lv[0];
+      CK(cudaMemcpyAsync(vbase(b, b.u), vbase(b, q->uhi), vbytes(q, b), cudaMemcpyDeviceToDevice, q->stream));
+      q->refine = false;
+    }
   }
   return GMT_OK;
 }

@@ -60,6 +60,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef TT_MINB
 #define TT_MINB 5
 #endif
+#ifndef TT_MINB_J
+#define TT_MINB_J 5
+#endif
 #ifndef TX_MINB
 #define TX_MINB 3
 #endif
@@ -67,7 +70,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #define TT_MINB2 3
 #endif
 template <int DPN, int MODE, int NRG, bool COARSE = false, bool FEXP = false>
-__global__ void __launch_bounds__(TT_X * TT_Y, TT_MINB)
+__global__ void __launch_bounds__(TT_X * TT_Y, (MODE == M_JACOBI && !COARSE && !FEXP) ? TT_MINB_J : TT_MINB)
 k_fine_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict__ u_all, ZMap zu,
              float* __restrict__ out_all, int n, int nz, const FineConsts P, double* __restrict__ part,
              ptrdiff_t cs, const uint8_t* __restrict__ flag, int ntx, int nty,
