@@ -6,7 +6,7 @@
 #include <nccl.h>
 
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cmath>
@@ -120,7 +120,7 @@ struct gmt_problem_s {
   double* hred = nullptr;  // pinned host mirror
   uint8_t* u8tmp = nullptr;
   uint8_t* tflag = nullptr;   // level-0 tile activity flags (k_tile_flags)
-  uint8_t* iflag = nullptr;   // level-0 interface-node flags (k_iface_flags)
+  uint8_t* iflag = nullptr;   // level-0 interface-node flags (k_material_scan)
   float* code = nullptr;      // level-0 node class: uniform voxel scale, or -1 (interface)
   int* ilist = nullptr;       // sorted interface-node list (static per material)
   int* elist = nullptr;       // sorted active-element (non-void voxel) list
@@ -492,18 +492,17 @@ int build_operators(gmt_problem p) {
   cudaStream_t st = p->stream;
   const int L = p->L;
   {
-    Prof prof(p, 6);
-    k_tile_flags<<<dim3(p->tntx, p->tnty, p->lv[0].nz), 128, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz,
-                                                                     p->tntx, p->tnty, p->tflag);
-    LAUNCHED(p);
-  }
-  {
-    // static interface-node list (sorted, deterministic)
+    // one pass over the material: node codes, interface / active-voxel flags,
+    // tile flags; then the static interface-node list (sorted, deterministic)
     const size_t total = p->lv[0].nodes;
     const int zlo = p->lv[0].dist ? -1 : 0, zhi = p->lv[0].nz + (p->lv[0].dist ? 1 : 0);
-    k_iface_flags<<<1184, 256, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, p->iflag, p->code, zlo, zhi);
-    LAUNCHED(p);
-    cub::CountingInputIterator<int> it(0);
+    {
+      Prof prof(p, 6);
+      k_material_scan<<<dim3(p->tntx, p->tnty), dim3(TT_X, TT_Y), 0, st>>>(
+          p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, zlo, zhi, p->code, p->iflag, p->eflag, p->tflag, p->tntx, p->tnty);
+      LAUNCHED(p);
+    }
+    thrust::counting_iterator<int> it(0);
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
     int cnt = 0;
     CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -511,8 +510,6 @@ int build_operators(gmt_problem p) {
     if (cnt != p->icount) drop_graph(p);   // grid size of the captured interface launch changes
     p->icount = cnt;
     // active elements (s != 0) for the C^H reduction
-    k_nonzero_flags<<<1184, 256, 0, st>>>(p->s, total, p->eflag);
-    LAUNCHED(p);
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->eflag, p->elist, p->icount_d, (int)total, st));
     CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -536,7 +533,7 @@ int build_operators(gmt_problem p) {
         LAUNCHED(p);
         k_neg_flags<<<1184, 256, 0, st>>>(b.ncode, b.nodes, p->iflag);
         LAUNCHED(p);
-        cub::CountingInputIterator<int> it(0);
+        thrust::counting_iterator<int> it(0);
         CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, b.ilist, p->icount_d, (int)b.nodes, st));
         int cnt = 0;
         CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1004,7 +1001,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   if ((rc = dalloc(p, (void**)&p->eflag, p->lv[0].nodes))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->icount_d, sizeof(int)))) return bail(rc);
   {
-    cub::CountingInputIterator<int> it(0);
+    thrust::counting_iterator<int> it(0);
     size_t bytes = 0;
     if (cub::DeviceSelect::Flagged(nullptr, bytes, it, p->iflag, p->ilist, p->icount_d, (int)p->lv[0].nodes) !=
         cudaSuccess)

@@ -712,29 +712,6 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
   }
 }
 
-// Interface nodes: those whose 8 incident voxels are not all equal (the
-// material interface).  flag = 1 per interface node (level 0).
-// Node codes are produced for planes [zlo, zhi) (ghost planes included when
-// slab-partitioned), interface flags for the local planes [0, nz).
-__global__ void k_iface_flags(const float* __restrict__ s, ZMap zs, int n, int nz, uint8_t* __restrict__ flag,
-                              float* __restrict__ code, int zlo, int zhi) {
-  const ptrdiff_t plane = (ptrdiff_t)n * n;
-  const ptrdiff_t total = plane * (zhi - zlo);
-  for (ptrdiff_t ii = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; ii < total; ii += (ptrdiff_t)gridDim.x * blockDim.x) {
-    const ptrdiff_t i = ii + (ptrdiff_t)zlo * plane;
-    const int x = (int)(ii % n), y = (int)((ii / n) % n), z = (int)(ii / plane) + zlo;
-    const int xm = wrapi(x - 1, n), ym = wrapi(y - 1, n), zm = zs(z - 1);
-    const float s0 = __ldg(s + (ptrdiff_t)zm * plane + (ptrdiff_t)ym * n + xm);
-    bool uni = true;
-#pragma unroll
-    for (int e = 1; e < 8; ++e) {
-      const ptrdiff_t idx = ((e >> 2) ? z : zm) * plane + (ptrdiff_t)(((e >> 1) & 1) ? y : ym) * n + ((e & 1) ? x : xm);
-      uni &= (__ldg(s + idx) == s0);
-    }
-    if (z >= 0 && z < nz) flag[i] = uni ? 0 : 1;
-    code[i] = uni ? s0 : -1.f;
-  }
-}
 
 // Coarse-level interface nodes (ncode -1) from a sorted list: stored
 // Galerkin stencil, f from memory.
@@ -769,6 +746,55 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
   }
   double nrm[2 * NR];
   op_epilogue<DPN, MODE>(true, out + node, cs, acc, fl, ui, D, omega, nrm, false);
+}
+
+// One pass over the material for the level-0 setup (replaces k_tile_flags +
+// the former per-node flag kernels): a CTA of 32 x 4 threads owns one tile
+// column and marches over the node planes [zlo, zhi), each thread keeping the
+// 4 voxels (x-1..x, y-1..y) of the previous plane in registers, so every
+// voxel is loaded once per thread instead of 8 (+ 33 x 5 per tile flag).
+// Outputs: node code (uniform scale or -1) for [zlo, zhi), interface flags
+// and active-voxel flags for [0, nz), tile flags for voxel planes [0, nz).
+__global__ void __launch_bounds__(TT_X * TT_Y)
+k_material_scan(const float* __restrict__ s, ZMap zs, int n, int nz, int zlo, int zhi,
+                float* __restrict__ code, uint8_t* __restrict__ iflag, uint8_t* __restrict__ eflag,
+                uint8_t* __restrict__ tflag, int ntx, int nty) {
+  const int x = blockIdx.x * TT_X + threadIdx.x, y = blockIdx.y * TT_Y + threadIdx.y;
+  const bool valid = x < n && y < n;
+  const int xc = valid ? x : 0, yc = valid ? y : 0;
+  const int xm = wrapi(xc - 1, n), ym = wrapi(yc - 1, n);
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
+  auto vox = [&](int zv, float (&v)[4]) {   // (xm,ym), (x,ym), (xm,y), (x,y) of voxel plane zv
+    const float* p = s + (ptrdiff_t)zs(zv) * plane;
+    v[0] = __ldg(p + (ptrdiff_t)ym * n + xm);
+    v[1] = __ldg(p + (ptrdiff_t)ym * n + xc);
+    v[2] = __ldg(p + (ptrdiff_t)yc * n + xm);
+    v[3] = __ldg(p + (ptrdiff_t)yc * n + xc);
+  };
+  float lo[4], hi[4];
+  vox(zlo - 1, lo);
+  for (int z = zlo; z < zhi; ++z) {
+    vox(z, hi);
+    const ptrdiff_t i = (ptrdiff_t)z * plane + (ptrdiff_t)yc * n + xc;
+    bool uni = true;
+#pragma unroll
+    for (int e = 1; e < 4; ++e) uni &= (lo[e] == lo[0]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) uni &= (hi[e] == lo[0]);
+    if (valid) code[i] = uni ? lo[0] : -1.f;
+    if (z >= 0 && z < nz) {
+      if (valid) {
+        iflag[i] = uni ? 0 : 1;
+        eflag[i] = hi[3] != 0.f ? 1 : 0;   // voxel (x, y, z)
+      }
+      const bool any = valid && (hi[0] != 0.f || hi[1] != 0.f || hi[2] != 0.f || hi[3] != 0.f);
+      const int tany = __syncthreads_or(any);
+      if (threadIdx.x == 0 && threadIdx.y == 0)
+        tflag[((ptrdiff_t)z * nty + blockIdx.y) * ntx + blockIdx.x] = tany ? 1 : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lo[e] = hi[e];
+  }
 }
 
 // The general (interface) path over the static interface-node list.

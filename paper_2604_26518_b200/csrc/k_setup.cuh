@@ -88,11 +88,6 @@ __global__ void k_neg_flags(const float* __restrict__ c, size_t n, uint8_t* __re
     flag[i] = c[i] < 0.f ? 1 : 0;
 }
 
-__global__ void k_nonzero_flags(const float* __restrict__ s, size_t n, uint8_t* __restrict__ flag) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    flag[i] = s[i] != 0.f ? 1 : 0;
-}
-
 __global__ void k_mask_inactive(const float* __restrict__ code, float* __restrict__ u, size_t nodes, int V) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes; i += (size_t)gridDim.x * blockDim.x)
     if (code[i] == 0.f)
