@@ -425,12 +425,8 @@ int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
   const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
   const Geo g = geo(bf.n, bf.nz);
   Prof prof(p, l == 0 ? 2 : 4);
-  if (l == 0)
-    k_prolong_add<DPN, true><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
-                                                                 p->s, p->zm(0), nullptr, bf.cs, bc.cs);
-  else
-    k_prolong_add<DPN, false><<<g.grid, g.block, 0, p->stream>>>(
-        e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, nullptr, p->zm(0), bf.ncode, bf.cs, bc.cs);
+  k_prolong_add<DPN><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
+                                                         l == 0 ? p->code : bf.ncode, bf.cs, bc.cs);
   LAUNCHED(p);
   return GMT_OK;
 }

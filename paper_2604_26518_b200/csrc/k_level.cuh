@@ -318,35 +318,43 @@ k_restrict(const float* __restrict__ r, ZMap zf, float* __restrict__ fc, int nc,
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  // per fine row (dy, dz): the aligned pair (2X, 2X+1) as one float2 and the
+  // left neighbour 2X-1 as a float (nf is even)
 #pragma unroll
   for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        const float w = (dx ? 0.5f : 1.f) * (dy ? 0.5f : 1.f) * (dz ? 0.5f : 1.f);
-        const ptrdiff_t i = (ptrdiff_t)zf(2 * Z + dz) * pf + (ptrdiff_t)wrapi(2 * Y + dy, nf) * nf +
-                            wrapi(2 * X + dx, nf);
-        if (actf && __ldg(actf + i) == 0.f) continue;   // R = P^T on active fine nodes only (App. E2)
-        float v[V];
-        load_node<DPN>(r + i, csf, v);
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = fmaf(w, v[k], acc[k]);
+    for (int dy = -1; dy <= 1; ++dy) {
+      const float w = (dy ? 0.5f : 1.f) * (dz ? 0.5f : 1.f);
+      const ptrdiff_t row = (ptrdiff_t)zf(2 * Z + dz) * pf + (ptrdiff_t)wrapi(2 * Y + dy, nf) * nf;
+      const ptrdiff_t ic = row + 2 * X, il = row + wrapi(2 * X - 1, nf);
+      // R = P^T on active fine nodes only (App. E2)
+      float wc = w, wr = 0.5f * w, wl = 0.5f * w;
+      if (actf) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(actf + ic));
+        wc = a.x != 0.f ? wc : 0.f;
+        wr = a.y != 0.f ? wr : 0.f;
+        wl = __ldg(actf + il) != 0.f ? wl : 0.f;
       }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float2 c = __ldg(reinterpret_cast<const float2*>(r + k * csf + ic));
+        const float l = __ldg(r + k * csf + il);
+        acc[k] = fmaf(wc, c.x, fmaf(wr, c.y, fmaf(wl, l, acc[k])));
+      }
+    }
   store_node<DPN>(fc + ((ptrdiff_t)Z * nc * nc + (ptrdiff_t)Y * nc + X), csc, acc);
 }
 
 // ---------------------------------------------------------------------------
 // App. E2 prolongation as a weighted gather, fused with the correction
 // u^l += P u^{l+1} (Alg. 1 line 10), on active fine nodes only (App. E2: the
-// stencil exists "for each active fine node").  Activity: level 0 -> any of
-// the 8 incident voxels non-void; level >= 1 -> nonzero stencil diagonal.
+// stencil exists "for each active fine node").  Activity from the fine node
+// codes (0 = every incident voxel / coarse element void).
 // ---------------------------------------------------------------------------
-template <int DPN, bool FINE0>
+template <int DPN>
 __global__ void __launch_bounds__(128)
 k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int nf, int nzf, int nc,
-              const float* __restrict__ s, ZMap zs, const float* __restrict__ Sdiag, ptrdiff_t csf,
-              ptrdiff_t csc) {
+              const float* __restrict__ act, ptrdiff_t csf, ptrdiff_t csc) {
   constexpr int V = Tr<DPN>::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -354,19 +362,7 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
   if (x >= nf || y >= nf) return;
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   const ptrdiff_t node = z * pf + (ptrdiff_t)y * nf + x;
-  bool act = false;
-  if (FINE0) {
-    const int xs0 = wrapi(x - 1, nf), ys0 = wrapi(y - 1, nf), zs0 = zs(z - 1);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const ptrdiff_t idx = ((k >> 2) ? z : zs0) * pf + (ptrdiff_t)(((k >> 1) & 1) ? y : ys0) * nf +
-                            ((k & 1) ? x : xs0);
-      act |= (__ldg(s + idx) != 0.f);
-    }
-  } else {
-    act = __ldg(Sdiag + node) != 0.f;
-  }
-  if (!act) return;
+  if (__ldg(act + node) == 0.f) return;
   const int X0 = x >> 1, Y0 = y >> 1, Zl = z >> 1;
   const int rx = x & 1, ry = y & 1, rz = z & 1;
   const int X1 = wrapi(X0 + 1, nc), Y1 = wrapi(Y0 + 1, nc), Z0 = zc(Zl), Z1 = zc(Zl + 1);
