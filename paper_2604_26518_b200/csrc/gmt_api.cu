@@ -78,6 +78,8 @@ struct LevelBuf {
   int tntx = 0, tnty = 0;
   int* ilist = nullptr;    // sorted interface nodes (ncode -1) of this coarse level
   int icount = 0;
+  float* Si = nullptr;     // their stencils in list order (k_gather_stencil)
+  size_t si_cap = 0;       // capacity of Si in nodes
   bool inj_pending = false;
 };
 
@@ -390,9 +392,9 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     if (b.icount == 0) return GMT_OK;
     const int nbi = (b.icount + 127) / 128;
     if (mode == M_JACOBI)
-      k_coarse_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
     else
-      k_coarse_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(b.S, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
   } else {
     const ZMap z = p->zm(l);
     switch (mode) {
@@ -482,6 +484,29 @@ int vcycle_dispatch(gmt_problem p) { return p->dpn == 3 ? vcycle_once<3>(p) : vc
 
 // ---------------------------------------------------------------- setup
 
+// Compact copies of the interface-node stencils of the tiled coarse levels
+// (after the stencils are assembled).  Reallocates when the list grows; the
+// captured V-cycle graph holds the pointer, so it is dropped then.
+int gather_iface_stencils(gmt_problem p) {
+  const int nent = 27 * p->dpn * p->dpn;
+  for (auto& b : p->lv) {
+    if (!b.tiled || b.icount == 0) continue;
+    if ((size_t)b.icount > b.si_cap) {
+      cudaFree(b.Si);
+      p->bytes -= b.si_cap * nent * sizeof(float);
+      b.Si = nullptr;
+      b.si_cap = 0;
+      const size_t cap = (size_t)b.icount + b.icount / 8 + 1024;
+      TRY(dalloc(p, (void**)&b.Si, cap * nent * sizeof(float)));
+      b.si_cap = cap;
+      drop_graph(p);
+    }
+    k_gather_stencil<<<1184, 256, 0, p->stream>>>(b.S, (ptrdiff_t)b.nodes, b.ilist, b.icount, nent, b.Si);
+    LAUNCHED(p);
+  }
+  return GMT_OK;
+}
+
 template <int DPN>
 int build_operators(gmt_problem p) {
   constexpr int ND = Tr<DPN>::ND;
@@ -563,6 +588,7 @@ int build_operators(gmt_problem p) {
     k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode, b.ncode, b.Kh);
     LAUNCHED(p);
   }
+  TRY(gather_iface_stencils(p));
   return GMT_OK;
 }
 
@@ -777,7 +803,7 @@ void free_all(gmt_problem p) {
     if (b.ecode) cudaFree(b.ecode - pl);
     if (b.ncode) cudaFree(b.ncode - pl);
     if (b.tflag) cudaFree(b.tflag - (size_t)b.tntx * b.tnty * TF_GLO);
-    cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.ilist);
+    cudaFree(b.Hl); cudaFree(b.Kh); cudaFree(b.ilist); cudaFree(b.Si);
   }
   for (float* v : {p->uhi, p->ulo, p->f0})
     if (v && !p->lv.empty()) cudaFree(vbase(p->lv[0], v));

@@ -713,8 +713,20 @@ k_fine_tiled2(const float* __restrict__ code, ZMap zs, const float* __restrict__
 }
 
 
+// Interface-node stencils in list order: Si[k * count + j] = S[k * nodes +
+// list[j]], so the sweep reads them coalesced (the list is sparse in the grid).
+__global__ void k_gather_stencil(const float* __restrict__ S, ptrdiff_t nodes, const int* __restrict__ list,
+                                 int count, int nent, float* __restrict__ Si) {
+  const ptrdiff_t total = (ptrdiff_t)count * nent;
+  for (ptrdiff_t t = blockIdx.x * (ptrdiff_t)blockDim.x + threadIdx.x; t < total;
+       t += (ptrdiff_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t % count), k = (int)(t / count);
+    Si[t] = __ldg(S + (ptrdiff_t)k * nodes + list[j]);
+  }
+}
+
 // Coarse-level interface nodes (ncode -1) from a sorted list: stored
-// Galerkin stencil, f from memory.
+// Galerkin stencil (compact, list order), f from memory.
 template <int DPN, int MODE>
 __global__ void __launch_bounds__(128)
 k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu, const float* __restrict__ f,
@@ -724,7 +736,7 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
   constexpr int NR = T::NR, V = T::V;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const ptrdiff_t plane = (ptrdiff_t)n * n, nodes = plane * nz;
+  const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t node = list[i];
   const int x = (int)(node % n), y = (int)((node / n) % n), z = (int)(node / plane);
   float acc[V], fl[V], ui[V], D[DPN];
@@ -738,7 +750,7 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
     for (int p = 0; p < DPN; ++p)
 #pragma unroll
       for (int q = 0; q < DPN; ++q) {
-        const float a = __ldg(S + (ptrdiff_t)((d * DPN + p) * DPN + q) * nodes + node);
+        const float a = __ldg(S + (ptrdiff_t)((d * DPN + p) * DPN + q) * count + i);
         if (d == 13 && p == q) D[p] = a;
 #pragma unroll
         for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, __ldg(u + (m * DPN + q) * cs + j), acc[m * DPN + p]);
