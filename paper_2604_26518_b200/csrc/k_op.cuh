@@ -74,11 +74,13 @@ __device__ __forceinline__ void node_uniform_pk(const Get& get, float c, float l
     const int i = 13 * 9 + p * 3 + p;
     D[p] = c * fmaf(lam, CT<3>::Hl(i), mu * CT<3>::Hm(i));
   }
-  f2 u2[3], a2[3];
+  // two accumulator sets (even / odd offsets): 6 independent FFMA2 chains
+  f2 u2[3], a2[3], b2[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     u2[q] = pk2(ui[q], ui[3 + q]);
     a2[q] = 0ull;
+    b2[q] = 0ull;
   }
 #pragma unroll
   for (int d = 14; d < 27; ++d) {
@@ -97,9 +99,12 @@ __device__ __forceinline__ void node_uniform_pk(const Get& get, float c, float l
         if (!hom_nz(d, p, q)) continue;
         const int i = d * 9 + p * 3 + q;
         const float h = fmaf(lam, CT<3>::Hl(i), mu * CT<3>::Hm(i));
-        a2[p] = fma2(pk2(h, h), w[q], a2[p]);
+        if (d & 1) b2[p] = fma2(pk2(h, h), w[q], b2[p]);
+        else a2[p] = fma2(pk2(h, h), w[q], a2[p]);
       }
   }
+#pragma unroll
+  for (int p = 0; p < 3; ++p) a2[p] = add2(a2[p], b2[p]);
   const f2 c2 = pk2(c, c);
 #pragma unroll
   for (int p = 0; p < 3; ++p) upk2(mul2(a2[p], c2), acc[p], acc[3 + p]);

@@ -1,5 +1,5 @@
-"""Parity at BASELINE.json's full size: the 512^3 elasticity gyroid (v_f 0.3,
-6 load cases) that bench.py times, in the launch configuration it times.
+"""Parity at BASELINE.json's full size: the 512^3 gyroid (v_f 0.3) that bench.py
+times (elasticity, 6 load cases; heat, 3), in the launch configuration it times.
 
 * One level-0 damped-Jacobi sweep through the tiled + interface kernels
   (levels = 1, one coarsest sweep: gmt_vcycle is then exactly that sweep) is
@@ -59,26 +59,28 @@ def _sample_nodes(s, rng):
     return sorted(nodes)
 
 
-def test_one_tiled_jacobi_sweep_sampled(workload):
+@pytest.mark.parametrize("kind", ["elastic", "thermal"])
+def test_one_tiled_jacobi_sweep_sampled(workload, kind):
     from paper_2604_26518_b200 import Problem
     s = workload
-    u0 = synth.initial_guess(N, 6, 3, seed=1, material=s)          # [m, c, z, y, x]
-    with Problem(s, physics="elastic", levels=1, coarse_sweeps=1, omega=OMEGA) as P:
+    ph = fem.Physics(kind)
+    om = OMEGA if kind == "elastic" else 0.6
+    u0 = synth.initial_guess(N, ph.nrhs, ph.dpn, seed=1, material=s)   # [m, c, z, y, x]
+    with Problem(s, physics=kind, levels=1, coarse_sweeps=1, omega=om) as P:
         assert P.levels == 1
         P.gmt_set_initial_guess(u0)
         P.gmt_vcycle(1)
         u1 = P.gmt_get_solution()
-    ph = fem.Physics("elastic")
     rng = np.random.default_rng(11)
     nodes = _sample_nodes(s, rng)
     Ku = fem.apply_K_at_nodes(s, ph, lambda x, y, z: u0[:, :, z, y, x], nodes)   # (len, M, dpn)
     f = fem.loads_at_nodes(s, ph, nodes)
     D = fem.diagonal_at_nodes(s, ph, nodes)                                        # (len, dpn)
-    want = np.zeros((len(nodes), 6, 3))
+    want = np.zeros((len(nodes), ph.nrhs, ph.dpn))
     got = np.zeros_like(want)
     for t, (x, y, z) in enumerate(nodes):
         if D[t].max() > 0:   # active node: u + omega D^-1 (f - K u); inactive nodes are returned as 0
-            want[t] = u0[:, :, z, y, x] + OMEGA * (f[t] - Ku[t]) / D[t][None, :]
+            want[t] = u0[:, :, z, y, x] + om * (f[t] - Ku[t]) / D[t][None, :]
         got[t] = u1[:, :, z, y, x]
     err = np.abs(got - want)
     assert err.max() <= 1e-5 * np.abs(want).max(), (err.max(), np.abs(want).max())
