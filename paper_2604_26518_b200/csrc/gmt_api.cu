@@ -106,6 +106,11 @@ struct gmt_problem_s {
   gmt_config cfg{};
   int dpn = 3, nr = 6, V = 18, L = 1, N = 0;
   cudaStream_t stream = nullptr;
+  // initial-guess uploads run on their own stream so they overlap the tail
+  // of the Galerkin build (ordered after the solution reset by ev_u_ready)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_u_ready = nullptr, ev_copy = nullptr;
+  bool u_ready_pending = false;
   bool own_stream = false;
   float* s = nullptr;  // material scales [z][y][x]
   std::vector<LevelBuf> lv;
@@ -190,9 +195,10 @@ inline float* vbase(const LevelBuf& b, float* v) { return v - (ptrdiff_t)b.gh * 
 inline size_t vbytes(gmt_problem p, const LevelBuf& b) { return (size_t)p->V * b.cs * sizeof(float); }
 
 // user layout [m][c][z][y][x] (component stride = nodes)  <->  internal layout
-int copy_in(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cudaMemcpyKind kind) {
+int copy_in(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cudaMemcpyKind kind,
+            cudaStream_t st = nullptr) {
   const size_t w = b.nodes * sizeof(float);
-  CK(cudaMemcpy2DAsync(dst, b.cs * sizeof(float), src, w, w, p->V, kind, p->stream));
+  CK(cudaMemcpy2DAsync(dst, b.cs * sizeof(float), src, w, w, p->V, kind, st ? st : p->stream));
   return GMT_OK;
 }
 int copy_out(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cudaMemcpyKind kind) {
@@ -628,8 +634,12 @@ int reset_solution(gmt_problem p) {
 }
 
 int rebuild(gmt_problem p) {
-  TRY(p->dpn == 3 ? build_operators<3>(p) : build_operators<1>(p));
+  // reset first: a following gmt_set_initial_guess upload only has to wait
+  // for the reset, not for the operator build
   TRY(reset_solution(p));
+  CK(cudaEventRecord(p->ev_u_ready, p->stream));
+  p->u_ready_pending = true;
+  TRY(p->dpn == 3 ? build_operators<3>(p) : build_operators<1>(p));
   return GMT_OK;
 }
 
@@ -813,6 +823,9 @@ void free_all(gmt_problem p) {
   cudaFree(p->iflag);
   if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->ev_u_ready) cudaEventDestroy(p->ev_u_ready);
+  if (p->ev_copy) cudaEventDestroy(p->ev_copy);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
 }
 
@@ -945,6 +958,10 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
       return bail(fail(GMT_ERR_CUDA, "cudaStreamCreate failed"));
     p->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_u_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_copy, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(GMT_ERR_CUDA, "stream / event creation failed"));
   p->lv.resize(L);
   const size_t V = p->V;
   // coarse levels at least this fine use the tiled sweep (env override for tests)
@@ -1148,8 +1165,19 @@ int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (p->grp) return g_set_initial_guess(p->grp, u, location);
   p->refine = false;
   LevelBuf& b = p->lv[0];
-  if (!u) CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
-  else TRY(copy_in(p, b, b.u, u, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice));
+  if (!u) {
+    CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
+    return GMT_OK;
+  }
+  // upload on the copy stream after everything that touched u, overlapping
+  // the operator build still queued on the problem stream
+  if (!p->u_ready_pending) CK(cudaEventRecord(p->ev_u_ready, p->stream));
+  p->u_ready_pending = false;
+  CK(cudaStreamWaitEvent(p->copy_stream, p->ev_u_ready, 0));
+  TRY(copy_in(p, b, b.u, u, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+              p->copy_stream));
+  CK(cudaEventRecord(p->ev_copy, p->copy_stream));
+  CK(cudaStreamWaitEvent(p->stream, p->ev_copy, 0));
   return GMT_OK;
 }
 
