@@ -572,7 +572,7 @@ int build_operators(gmt_problem p) {
     LevelBuf& b = p->lv[1];
     const Geo g = geo(b.n, b.nz);
     Prof prof(p, 6);
-    k_stencil_l1<DPN><<<g.grid, g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz,
+    k_stencil_l1<DPN><<<dim3(g.grid.x, g.grid.y, g.grid.z * 3), g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz,
                                                   (float)p->ed.lam, (float)p->ed.mu, b.ncode);
     LAUNCHED(p);
   }

@@ -142,19 +142,23 @@ __device__ __forceinline__ void l1_block(const float (&sv)[64], float lam, float
       S[((D * DPN + p) * DPN + q) * nodes + node] = CT<DPN>::two ? fmaf(lam, Al[p][q], mu * Am[p][q]) : lam * Al[p][q];
 }
 
-template <int DPN, int... Ds>
-__device__ __forceinline__ void l1_all(std::integer_sequence<int, Ds...>, const float (&sv)[64], float lam,
-                                       float mu, float* __restrict__ S, ptrdiff_t nodes, ptrdiff_t node) {
-  (l1_block<DPN, Ds>(sv, lam, mu, S, nodes, node), ...);
+// The 9 offsets of one dz plane (g = dz + 1): a CTA runs one group's code,
+// a third of the 27 unrolled blocks, which keeps the instruction cache warm.
+template <int DPN, int G, int... Ds>
+__device__ __forceinline__ void l1_group(std::integer_sequence<int, Ds...>, const float (&sv)[64], float lam,
+                                         float mu, float* __restrict__ S, ptrdiff_t nodes, ptrdiff_t node) {
+  (l1_block<DPN, 9 * G + Ds>(sv, lam, mu, S, nodes, node), ...);
 }
 
+// grid.z = 3 * nzc: block (., ., 3 Z + g) computes the offsets of dz = g - 1
+// of plane Z, so consecutive CTAs share one group's code.
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc,
              float lam, float mu, const float* __restrict__ ncd) {
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int Z = blockIdx.z;
+  const int Z = blockIdx.z / 3, grp = blockIdx.z % 3;
   if (X >= nc || Y >= nc) return;
   const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
   const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
@@ -171,7 +175,9 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
       for (int fx = 0; fx < 4; ++fx) sv[(fz * 4 + fy) * 4 + fx] = __ldg(s + yo + wrapi(2 * X - 2 + fx, nf));
     }
   }
-  l1_all<DPN>(std::make_integer_sequence<int, 27>{}, sv, lam, mu, S, nodes, node);
+  if (grp == 0) l1_group<DPN, 0>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
+  else if (grp == 1) l1_group<DPN, 1>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
+  else l1_group<DPN, 2>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
 }
 
 // Level-2 Galerkin element matrices straight from the material:
@@ -243,12 +249,16 @@ __global__ void __launch_bounds__(576)
 k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, int nzc, const WConsts Wt,
                 const float* __restrict__ ecf, const float* __restrict__ ecc, const float* __restrict__ Khf) {
   constexpr int ND = Tr<DPN>::ND;
-  __shared__ float Kc[ND * ND], Tm[ND * ND];
+  __shared__ float Kc[ND * ND], Tm[ND * ND], Ws[512];
   const int t = threadIdx.x;
   const int r = t / ND, c = t % ND;
   const int A = r / DPN, p = r % DPN, B = c / DPN, q = c % DPN;
   const int E = blockIdx.x;
   if (__ldg(ecc + E) >= 0.f) return;            // uniform element: c Khom_l, nothing stored
+  // prolongation weights in shared memory: the per-thread corner index B / A
+  // makes constant-bank reads divergent (serialised LDC, MIO throttle)
+  for (int i = t; i < 512; i += blockDim.x) Ws[i] = Wt.W[i];
+  __syncthreads();
   const int X = E % nc, Y = (E / nc) % nc, Z = E / (nc * nc);
   const int nfr = 2 * nc;
   float acc = 0.f;
@@ -260,11 +270,11 @@ k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, 
     __syncthreads();
     float tv = 0.f;   // T[(a p)][(B q)], here r = (a p)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) tv = fmaf(Wt.W[(j * 8 + b) * 8 + B], Kc[r * ND + b * DPN + q], tv);
+    for (int b = 0; b < 8; ++b) tv = fmaf(Ws[(j * 8 + b) * 8 + B], Kc[r * ND + b * DPN + q], tv);
     Tm[t] = tv;
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 8; ++a) acc = fmaf(Wt.W[(j * 8 + a) * 8 + A], Tm[(a * DPN + p) * ND + c], acc);
+    for (int a = 0; a < 8; ++a) acc = fmaf(Ws[(j * 8 + a) * 8 + A], Tm[(a * DPN + p) * ND + c], acc);
     __syncthreads();
   }
   dst[(ptrdiff_t)E * (ND * ND) + t] = acc;
