@@ -131,6 +131,7 @@ struct gmt_problem_s {
   float* code = nullptr;      // level-0 node class: uniform voxel scale, or -1 (interface)
   int* ilist = nullptr;       // sorted interface-node list (static per material)
   int* elist = nullptr;       // sorted active-element (non-void voxel) list
+  int* l2list = nullptr;      // non-uniform level-2 elements (Galerkin build)
   uint8_t* eflag = nullptr;
   int ecount = 0;
   int* icount_d = nullptr;
@@ -513,6 +514,17 @@ int gather_iface_stencils(gmt_problem p) {
   return GMT_OK;
 }
 
+// Sorted list of the entries with code < 0 (deterministic), count to the host.
+int select_neg(gmt_problem p, const float* code, size_t n, int* list, int* count) {
+  k_neg_flags<<<1184, 256, 0, p->stream>>>(code, n, p->iflag);
+  LAUNCHED(p);
+  thrust::counting_iterator<int> it(0);
+  CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, list, p->icount_d, (int)n, p->stream));
+  CK(cudaMemcpyAsync(count, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return GMT_OK;
+}
+
 template <int DPN>
 int build_operators(gmt_problem p) {
   constexpr int ND = Tr<DPN>::ND;
@@ -578,18 +590,26 @@ int build_operators(gmt_problem p) {
   }
   for (int l = 2; l < L; ++l) {
     LevelBuf& b = p->lv[l];
-    const unsigned nelem = (unsigned)b.nodes;
     Prof prof(p, 6);
     if (l == 2) {
+      // compact list of the non-uniform level-2 elements (the rest are c Khom_2)
+      int cnt = 0;
+      TRY(select_neg(p, b.ecode, b.nodes, p->l2list, &cnt));
       constexpr int TE = 16;
-      const unsigned ntile = (nelem + TE - 1) / TE;
-      const unsigned grid = std::min(ntile, (unsigned)(148 * (DPN == 3 ? 1 : 16)));
-      k_elem_l2<DPN, TE><<<grid, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g, b.Ke, b.n, b.nz, b.ecode);
+      const unsigned ntile = (unsigned)((cnt + TE - 1) / TE);
+      const unsigned grid = std::max(1u, std::min(ntile, (unsigned)(148 * (DPN == 3 ? 1 : 16))));
+      k_elem_l2<DPN, TE><<<grid, ND * ND, 0, st>>>(p->s, p->zm(0), p->lv[0].n, p->M2g, b.Ke, b.n, b.nz, p->l2list,
+                                                   cnt);
+      LAUNCHED(p);
     } else {
-      k_galerkin_elem<DPN><<<nelem, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc, p->lv[l - 1].ecode,
-                                                     b.ecode, p->lv[l - 1].Kh);
+      int cnt = 0;
+      TRY(select_neg(p, b.ecode, b.nodes, p->l2list, &cnt));
+      if (cnt > 0) {
+        k_galerkin_elem<DPN><<<cnt, ND * ND, 0, st>>>(p->lv[l - 1].Ke, b.Ke, b.n, b.nz, p->wc, p->lv[l - 1].ecode,
+                                                     p->l2list, p->lv[l - 1].Kh);
+        LAUNCHED(p);
+      }
     }
-    LAUNCHED(p);
     const Geo g = geo(b.n, b.nz);
     k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode, b.ncode, b.Kh);
     LAUNCHED(p);
@@ -821,7 +841,7 @@ void free_all(gmt_problem p) {
   cudaFree(p->M1g); cudaFree(p->M2g);
   if (p->tflag) cudaFree(p->tflag - (size_t)p->tntx * p->tnty * TF_GLO);
   cudaFree(p->iflag);
-  if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->l2list); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->ev_u_ready) cudaEventDestroy(p->ev_u_ready);
@@ -1037,6 +1057,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   p->code += pl0;   // node codes of planes -1 .. nz
   if ((rc = dalloc(p, (void**)&p->ilist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->elist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
+  if (L >= 3 && (rc = dalloc(p, (void**)&p->l2list, p->lv[2].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->eflag, p->lv[0].nodes))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->icount_d, sizeof(int)))) return bail(rc);
   {

@@ -190,12 +190,11 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
 template <int DPN, int TE>
 __global__ void __launch_bounds__(Tr<DPN>::ND * Tr<DPN>::ND)
 k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict__ M2,
-          float* __restrict__ dst, int n2, int nz2, const float* __restrict__ ecd) {
+          float* __restrict__ dst, int n2, int nz2, const int* __restrict__ list, int count) {
   constexpr int NT = Tr<DPN>::ND * Tr<DPN>::ND;
   __shared__ __align__(16) float sg[64][TE];
   const int t = threadIdx.x;
-  const ptrdiff_t nelem = (ptrdiff_t)n2 * n2 * nz2;
-  const ptrdiff_t ntile = (nelem + TE - 1) / TE;
+  const ptrdiff_t ntile = (count + TE - 1) / TE;   // tiles of the non-uniform element list
   float m[64];
 #pragma unroll
   for (int g = 0; g < 64; ++g) m[g] = __ldg(M2 + g * NT + t);
@@ -204,9 +203,9 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
     bool any = false;
     for (int i = t; i < 64 * TE; i += NT) {
       const int e = i % TE, g = i / TE;
-      const ptrdiff_t E = E0 + e;
       float v = 0.f;
-      if (E < nelem && __ldg(ecd + E) < 0.f) {   // only non-uniform elements are stored
+      if (E0 + e < count) {
+        const ptrdiff_t E = __ldg(list + E0 + e);
         const int X = (int)(E % n2), Y = (int)((E / n2) % n2), Z = (int)(E / ((ptrdiff_t)n2 * n2));
         const int gx = g & 3, gy = (g >> 2) & 3, gz = g >> 4;
         v = __ldg(s + ((ptrdiff_t)zs(4 * Z + gz) * n0 + 4 * Y + gy) * n0 + 4 * X + gx);
@@ -234,7 +233,7 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
     if (tile_any) {
 #pragma unroll
       for (int e = 0; e < TE; ++e)
-        if (E0 + e < nelem && __ldg(ecd + E0 + e) < 0.f) dst[(E0 + e) * NT + t] = acc[e];
+        if (E0 + e < count) dst[(ptrdiff_t)__ldg(list + E0 + e) * NT + t] = acc[e];
     }
     __syncthreads();
   }
@@ -247,14 +246,13 @@ k_elem_l2(const float* __restrict__ s, ZMap zs, int n0, const float* __restrict_
 template <int DPN>
 __global__ void __launch_bounds__(576)
 k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, int nzc, const WConsts Wt,
-                const float* __restrict__ ecf, const float* __restrict__ ecc, const float* __restrict__ Khf) {
+                const float* __restrict__ ecf, const int* __restrict__ list, const float* __restrict__ Khf) {
   constexpr int ND = Tr<DPN>::ND;
   __shared__ float Kc[ND * ND], Tm[ND * ND], Ws[512];
   const int t = threadIdx.x;
   const int r = t / ND, c = t % ND;
   const int A = r / DPN, p = r % DPN, B = c / DPN, q = c % DPN;
-  const int E = blockIdx.x;
-  if (__ldg(ecc + E) >= 0.f) return;            // uniform element: c Khom_l, nothing stored
+  const int E = __ldg(list + blockIdx.x);       // non-uniform coarse elements only (uniform: c Khom_l)
   // prolongation weights in shared memory: the per-thread corner index B / A
   // makes constant-bank reads divergent (serialised LDC, MIO throttle)
   for (int i = t; i < 512; i += blockDim.x) Ws[i] = Wt.W[i];
