@@ -149,6 +149,7 @@ struct gmt_problem_s {
   float *uhi = nullptr, *ulo = nullptr, *f0 = nullptr;
   const float* f0_active = nullptr;   // explicit level-0 rhs during a refinement V-cycle
   bool refine = false;
+  bool defect_valid = false;          // f0 holds the defect of the current hi + lo (residual norms computed it)
   int refine_mode = 0;                // 0 auto (gmt_solve switches at the fp32 floor), 1 off, 2 always
   // kernel accounting and live profiling
   long long launches = 0;         // kernels executed (graph replays included)
@@ -754,6 +755,7 @@ int refine_enter(gmt_problem p) {
   CK(cudaMemcpyAsync(vbase(b, p->uhi), vbase(b, b.u), vbytes(p, b), cudaMemcpyDeviceToDevice, p->stream));
   CK(cudaMemsetAsync(vbase(b, p->ulo), 0, vbytes(p, b), p->stream));
   p->refine = true;
+  p->defect_valid = false;
   return GMT_OK;
 }
 
@@ -775,6 +777,7 @@ int refine_defect(gmt_problem p, double* ar, double* af) {
     TRY(reduce(p, l0_partials<DPN>(p, true), 2 * NR));
     for (int m = 0; m < NR; ++m) if (ar) ar[m] = std::sqrt(p->hred[m]);
   }
+  p->defect_valid = true;
   return GMT_OK;
 }
 
@@ -784,7 +787,9 @@ int refine_defect(gmt_problem p, double* ar, double* af) {
 template <int DPN>
 int refine_cycle(gmt_problem p) {
   LevelBuf& b = p->lv[0];
-  TRY(refine_defect<DPN>(p, nullptr, nullptr));
+  // the defect of the current solution is often already in f0 (gmt_solve
+  // computes it for the residual norms right before the next cycle)
+  if (!p->defect_valid) TRY(refine_defect<DPN>(p, nullptr, nullptr));
   CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
   p->f0_active = p->f0;
   const int rc = vcycle_once<DPN>(p);
@@ -792,6 +797,7 @@ int refine_cycle(gmt_problem p) {
   TRY(rc);
   k_refine_update<<<1184, 256, 0, p->stream>>>(p->code, p->uhi, p->ulo, b.u, (ptrdiff_t)b.nodes, p->V, b.cs);
   LAUNCHED(p);
+  p->defect_valid = false;
   return GMT_OK;
 }
 
