@@ -273,7 +273,7 @@ int ch_grid() {
     int per = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_effective_tensor<DPN>, CH_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, GMT_CH_KERNEL<DPN>, CH_THREADS, 0);
     g = std::max(1, per) * std::max(1, sms);
   }
   return g;
@@ -684,10 +684,10 @@ template <int DPN>
 int effective_tensor(gmt_problem p, const float* u, double* CH) {
   constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
   const LevelBuf& b = p->lv[0];
-  const int nblk = std::max(1, std::min((2 * p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
+  const int nblk = std::max(1, std::min((GMT_CH_ITEMS * p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
   {
     Prof prof(p, 7);
-    k_effective_tensor<DPN><<<nblk, CH_THREADS, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
+    GMT_CH_KERNEL<DPN><<<nblk, CH_THREADS, 0, p->stream>>>(p->s, u, p->zm(0), b.n, b.nz, (float)p->ed.lam,
                                                          (float)p->ed.mu, p->part, b.cs, p->elist,
                                                          p->ecount);
     LAUNCHED(p);
