@@ -111,7 +111,12 @@ GMT_API int gmt_create(const gmt_config* cfg, const void* material, int material
 GMT_API int gmt_set_material(gmt_problem p, const void* material, int dtype, int location);
 
 /* Alg. 2 line 1: u^1 <- u_hat^1.  u: finest-level vector (layout above) or
- * NULL for zero. */
+ * NULL for zero.  Only active nodes (nodes touching a nonzero voxel, Sec.
+ * 4.1.1) carry unknowns: values of u at inactive nodes are ignored (a device
+ * buffer is copied at active nodes only; gmt_get_solution reports inactive
+ * nodes as 0).  The upload is stream-ordered; the caller keeps u valid until
+ * the next call that synchronises (gmt_homogenize, gmt_residual_norms,
+ * gmt_get_solution to host, gmt_sync).  Errors: GMT_ERR_ARG, GMT_ERR_CUDA. */
 GMT_API int gmt_set_initial_guess(gmt_problem p, const float* u, int location);
 
 /* Alg. 2 line 6: u^{l} <- e_hat^{l} instead of 0 for level l in [1, L-1]

@@ -111,6 +111,9 @@ struct gmt_problem_s {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_u_ready = nullptr, ev_copy = nullptr;
   bool u_ready_pending = false;
+  // level-0 solution reset deferred by gmt_set_material until the next public
+  // call (set_device): a following gmt_set_initial_guess overwrites it anyway
+  bool u0_stale = false, u0_zeroed = false;
   bool own_stream = false;
   float* s = nullptr;  // material scales [z][y][x]
   std::vector<LevelBuf> lv;
@@ -211,6 +214,10 @@ int copy_out(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cud
 
 int set_device(gmt_problem p) {
   CK(cudaSetDevice(p->cfg.device));
+  if (p->u0_stale) {
+    p->u0_stale = false;
+    CK(cudaMemsetAsync(vbase(p->lv[0], p->lv[0].u), 0, vbytes(p, p->lv[0]), p->stream));
+  }
   return GMT_OK;
 }
 
@@ -541,6 +548,8 @@ int build_operators(gmt_problem p) {
       k_material_scan<<<dim3(p->tntx, p->tnty), dim3(TT_X, TT_Y), 0, st>>>(
           p->s, p->zm(0), p->lv[0].n, p->lv[0].nz, zlo, zhi, p->code, p->iflag, p->eflag, p->tflag, p->tntx, p->tnty);
       LAUNCHED(p);
+      // a following device initial-guess upload needs the node codes (and the reset before them)
+      CK(cudaEventRecord(p->ev_u_ready, st));
     }
     thrust::counting_iterator<int> it(0);
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
@@ -646,10 +655,18 @@ int upload_material(gmt_problem p, const void* material, int dtype, int location
 // nodes and prolongation writes active fine nodes only.  Void warps therefore
 // skip reads and writes entirely, and a new material needs no buffer clearing
 // beyond resetting the solution.
-int reset_solution(gmt_problem p) {
-  for (auto& b : p->lv) {
-    CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
+int reset_solution(gmt_problem p, bool defer0 = false) {
+  for (size_t l = 0; l < p->lv.size(); ++l) {
+    LevelBuf& b = p->lv[l];
     b.inj_pending = false;
+    // level 0 of a single-device problem: once zeroed in full (padding
+    // included), later resets are deferred to the next public call
+    if (l == 0 && defer0 && !p->grp && p->u0_zeroed) {
+      p->u0_stale = true;
+      continue;
+    }
+    CK(cudaMemsetAsync(vbase(b, b.u), 0, vbytes(p, b), p->stream));
+    if (l == 0) p->u0_zeroed = true;
   }
   return GMT_OK;
 }
@@ -657,7 +674,7 @@ int reset_solution(gmt_problem p) {
 int rebuild(gmt_problem p) {
   // reset first: a following gmt_set_initial_guess upload only has to wait
   // for the reset, not for the operator build
-  TRY(reset_solution(p));
+  TRY(reset_solution(p, true));
   CK(cudaEventRecord(p->ev_u_ready, p->stream));
   p->u_ready_pending = true;
   TRY(p->dpn == 3 ? build_operators<3>(p) : build_operators<1>(p));
@@ -1188,6 +1205,7 @@ int gmt_set_material(gmt_problem p, const void* material, int dtype, int locatio
 
 int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
+  p->u0_stale = false;   // both branches below overwrite every level-0 value
   TRY(set_device(p));
   if (p->grp) return g_set_initial_guess(p->grp, u, location);
   p->refine = false;
@@ -1201,8 +1219,12 @@ int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (!p->u_ready_pending) CK(cudaEventRecord(p->ev_u_ready, p->stream));
   p->u_ready_pending = false;
   CK(cudaStreamWaitEvent(p->copy_stream, p->ev_u_ready, 0));
-  TRY(copy_in(p, b, b.u, u, location == GMT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-              p->copy_stream));
+  if (location == GMT_DEVICE) {
+    k_copy_active<<<1184, 256, 0, p->copy_stream>>>(p->code, u, b.u, b.nodes, b.cs, p->V);
+    LAUNCHED(p);
+  } else {
+    TRY(copy_in(p, b, b.u, u, cudaMemcpyHostToDevice, p->copy_stream));
+  }
   CK(cudaEventRecord(p->ev_copy, p->copy_stream));
   CK(cudaStreamWaitEvent(p->stream, p->ev_copy, 0));
   return GMT_OK;

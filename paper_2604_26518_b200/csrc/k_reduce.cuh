@@ -49,6 +49,10 @@ k_reduce_stage(const double* __restrict__ part, int nblk, int nv, double* __rest
 // per-element fp32 sums are accumulated in fp64 per thread, then one block
 // partial of the upper triangle.
 constexpr int CH_THREADS = 64;
+#ifndef GMT_CH_UNROLL
+#define GMT_CH_UNROLL 2
+#endif
+constexpr int CH_UNROLL = GMT_CH_UNROLL;   // load cases staged per step (gathers in flight)
 
 // Kept for A/B (build with -DGMT_CH_GAUSS); the default is the Walsh form below.
 template <int DPN>
@@ -276,7 +280,7 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
       // stage per load case: 0..5 constant-mode strains e_m - eps_0 (Voigt
       // 11,22,33,23,13,12), then h_xy[c] 6..8, h_xz[c] 9..11, h_yz[c] 12..14,
       // h_xyz[c] 15..17 of the three displacement components.
-#pragma unroll 1
+#pragma unroll CH_UNROLL
       for (int m = 0; m < NR; ++m) {
         float h[3][7];
 #pragma unroll

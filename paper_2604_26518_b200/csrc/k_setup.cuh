@@ -94,6 +94,27 @@ __global__ void k_mask_inactive(const float* __restrict__ code, float* __restric
       for (int k = 0; k < V; ++k) u[k * nodes + i] = 0.f;
 }
 
+// Device-resident initial guess (Alg. 2 line 1): copy the active nodes only
+// (code != 0).  Values at inactive nodes never influence active ones (see
+// reset_solution) and gmt_get_solution reports them as 0, so they are left as
+// they are -- the copy reads ~the active fraction of the guess instead of all
+// of it.  src is [V][nodes], dst [V][cs].
+__global__ void k_copy_active(const float* __restrict__ code, const float* __restrict__ src,
+                              float* __restrict__ dst, size_t nodes, ptrdiff_t cs, int V) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes; i += (size_t)gridDim.x * blockDim.x) {
+    if (code[i] == 0.f) continue;
+    int k = 0;
+    for (; k + 6 <= V; k += 6) {
+      float v[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) v[j] = __ldcs(src + (size_t)(k + j) * nodes + i);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) dst[(ptrdiff_t)(k + j) * cs + (ptrdiff_t)i] = v[j];
+    }
+    for (; k < V; ++k) dst[(ptrdiff_t)k * cs + (ptrdiff_t)i] = __ldcs(src + (size_t)k * nodes + i);
+  }
+}
+
 __global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     out[i] = in[i] ? 1.f : 0.f;

@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmt.so")
+# GMT_LIB selects an in-tree build variant for A/B timing (scripts/ab_lib.sh)
+LIB_PATH = os.environ.get("GMT_LIB") or os.path.join(_HERE, "libgmt.so")
 
 GMT_OK = 0
 PHYSICS = {"elastic": 0, "thermal": 1}
