@@ -281,6 +281,19 @@ def test_u8_material_and_degenerate_inputs():
         assert np.all(P.gmt_get_solution() == 0)
         rel, ar, af = P.gmt_residual_norms()
         assert np.all(ar == 0) and np.all(af == 0)
+        assert np.all(P.gmt_homogenize() == 0)                       # no active element
+    # solid cube: u stays 0 (f = 0) and C^H is the base tensor (App. F1 with u = 0)
+    lam, mu = 0.3 / (1.3 * 0.4), 1.0 / 2.6
+    C0 = np.zeros((6, 6))
+    C0[:3, :3] = lam
+    C0[np.arange(3), np.arange(3)] += 2 * mu
+    C0[np.arange(3, 6), np.arange(3, 6)] = mu
+    with _problem(np.ones((8, 8, 8), np.float32), "elastic", 2) as P:
+        P.gmt_vcycle(1)
+        assert np.abs(P.gmt_homogenize() - C0).max() <= 1e-6
+    with _problem(np.ones((8, 8, 8), np.float32), "thermal", 2, kappa=2.5) as P:
+        P.gmt_vcycle(1)
+        assert np.abs(P.gmt_homogenize() - 2.5 * np.eye(3)).max() <= 1e-6
     # single level (L = 1): smoothing only; 2^3 minimum grid
     s2 = synth.random_occupancy(2, 0.6, seed=1)
     ph = fem.Physics("thermal")
