@@ -47,9 +47,9 @@ struct FineConsts {      // level 0 (material-driven) operator: material scalars
 // Block-wide reduction of NV doubles per thread; thread 0 of the block
 // writes the NV block sums to out[0..NV).  Fixed summation order
 // (deterministic).  blockDim.x * blockDim.y * blockDim.z <= 1024.
-template <int NV>
+template <int NV, int MAXW = 32>
 __device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* __restrict__ out) {
-  __shared__ double sh[32][NV];
+  __shared__ double sh[MAXW][NV];   // one row per warp of the CTA (MAXW >= warps)
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nthr = blockDim.x * blockDim.y * blockDim.z;
   const int lane = tid & 31, warp = tid >> 5;
@@ -65,7 +65,7 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* __re
     const int nw = (nthr + 31) >> 5;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      double a = lane < nw ? sh[lane][k] : 0.0;
+      double a = lane < nw && lane < MAXW ? sh[lane < MAXW ? lane : 0][k] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
       if (lane == 0) out[k] = a;

@@ -203,8 +203,11 @@ k_effective_tensor_gauss(const float* __restrict__ s, const float* __restrict__ 
 // bilinear modes collapse to (lam + 4 mu)/144 sum_c h_xyz,c h'_xyz,c.
 // One thread per active element; the 18 per-case values are staged in shared
 // memory (thread-fastest, conflict-free) for the NR(NR+1)/2 Gram sums.
+#ifndef GMT_CH_MINB
+#define GMT_CH_MINB 6
+#endif
 template <int DPN>
-__global__ void __launch_bounds__(CH_THREADS, 6)
+__global__ void __launch_bounds__(CH_THREADS, GMT_CH_MINB)
 k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMap zu, int n, int nz,
                    float lam, float mu, double* __restrict__ part, ptrdiff_t cs,
                    const int* __restrict__ elist, int ecount) {
@@ -316,34 +319,53 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
           for (int k = m; k < NR; ++k) qf[qi++] = pk2(fmaf(b2, Bv[k][2], fmaf(b1, Bv[k][1], b0 * Bv[k][0])), 0.f);
         }
       }
-      // chunk A: constant mode | s_z mode (linear, 1/48) in the two lanes
+      // chunk A: constant mode | s_z mode (linear, 1/48) in the two lanes;
+      // normal strains (A1, carry the trace) and shears (A2) separately
       {
-        f2 E[NR][6];
+        f2 E[NR][3];
 #pragma unroll
         for (int m = 0; m < NR; ++m) {
           E[m][0] = pk2(H(m, 0), H(m, 9));              // eps11 | h_xz,1
           E[m][1] = pk2(H(m, 1), H(m, 13));             // eps22 | h_yz,2
           E[m][2] = pk2(H(m, 2), 0.f);                  // eps33 | -
-          E[m][3] = pk2(H(m, 3), H(m, 14));             // gam23 | h_yz,3
-          E[m][4] = pk2(H(m, 4), H(m, 11));             // gam13 | h_xz,3
-          E[m][5] = pk2(H(m, 5), H(m, 12) + H(m, 10));  // gam12 | h_yz,1 + h_xz,2
         }
-        const f2 l2 = pk2(lam, lam * (1.f / 48.f)), m2 = pk2(2.f * mu, 2.f * mu * (1.f / 48.f)),
-                 m1 = pk2(mu, mu * (1.f / 48.f));
+        const f2 l2 = pk2(lam, lam * (1.f / 48.f)), m2 = pk2(2.f * mu, 2.f * mu * (1.f / 48.f));
         int qi = 0;
 #pragma unroll
         for (int m = 0; m < NR; ++m) {
-          f2 sg[6];
+          f2 sg[3];
           const f2 lt = mul2(l2, add2(add2(E[m][0], E[m][1]), E[m][2]));
 #pragma unroll
           for (int i = 0; i < 3; ++i) sg[i] = fma2(m2, E[m][i], lt);
 #pragma unroll
-          for (int i = 3; i < 6; ++i) sg[i] = mul2(m1, E[m][i]);
+          for (int k = m; k < NR; ++k) {
+            f2 a = qf[qi];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) a = fma2(sg[i], E[k][i], a);
+            qf[qi++] = a;
+          }
+        }
+      }
+      {
+        f2 E[NR][3];
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          E[m][0] = pk2(H(m, 3), H(m, 14));             // gam23 | h_yz,3
+          E[m][1] = pk2(H(m, 4), H(m, 11));             // gam13 | h_xz,3
+          E[m][2] = pk2(H(m, 5), H(m, 12) + H(m, 10));  // gam12 | h_yz,1 + h_xz,2
+        }
+        const f2 m1 = pk2(mu, mu * (1.f / 48.f));
+        int qi = 0;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+          f2 sg[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) sg[i] = mul2(m1, E[m][i]);
 #pragma unroll
           for (int k = m; k < NR; ++k) {
             f2 a = qf[qi];
 #pragma unroll
-            for (int i = 0; i < 6; ++i) a = fma2(sg[i], E[k][i], a);
+            for (int i = 0; i < 3; ++i) a = fma2(sg[i], E[k][i], a);
             qf[qi++] = a;
           }
         }
@@ -389,7 +411,7 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
       }
     }
   }
-  block_reduce_store<NQ>(q, part + (ptrdiff_t)blockIdx.x * NQ);
+  block_reduce_store<NQ, CH_THREADS / 32>(q, part + (ptrdiff_t)blockIdx.x * NQ);
 }
 
 #ifdef GMT_CH_GAUSS
