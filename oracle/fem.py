@@ -311,3 +311,33 @@ def from_node_layout(a: np.ndarray) -> np.ndarray:
     """[z, y, x, m, c] -> (ndof, M)."""
     n, M, dpn = a.shape[0], a.shape[3], a.shape[4]
     return a.transpose(0, 1, 2, 4, 3).reshape(n ** 3 * dpn, M).astype(np.float64)
+
+
+def effective_tensor_planes(s: np.ndarray, phys: Physics, u_plane, z0: int, z1: int) -> np.ndarray:
+    """The App. F1 / F2 sum of ``effective_tensor`` restricted to the elements
+    of voxel planes ez in [z0, z1), NOT divided by |Omega|:
+        sum_{e: z0 <= ez < z1} (x_0^i - u_e^i)^T (s_e K_e) (x_0^j - u_e^j).
+    Summing it over a partition of the planes and dividing by N^3 gives
+    C^H; it exists so that fields too large for the (ndof, M) layout (512^3)
+    can be evaluated one plane at a time.  ``u_plane(z)`` returns the nodal
+    values of node plane z (periodic) as an array [y, x, m, c]."""
+    n = s.shape[0]
+    dpn, M = phys.dpn, phys.nrhs
+    out = np.zeros((M, M))
+    for ez in range(z0, z1):
+        se = s[ez % n].astype(np.float64).reshape(-1)           # element (ex, ey) at ey * n + ex
+        act = se != 0
+        if not act.any():
+            continue
+        ue = np.zeros((n * n, 8 * dpn, M))
+        planes = {kz: np.asarray(u_plane((ez + kz) % n), dtype=np.float64) for kz in (0, 1)}
+        for k in range(8):
+            kx, ky, kz = CORNERS[k]
+            # corner k of element (ex, ey) is node ((ex + kx) mod n, (ey + ky) mod n)
+            v = np.roll(planes[kz], shift=(-ky, -kx), axis=(0, 1)).reshape(n * n, M, dpn)
+            ue[:, k * dpn:(k + 1) * dpn, :] = v.transpose(0, 2, 1)
+        d = phys.X0[None, :, :] - ue[act]                       # (ne, 8dpn, M)
+        Kd = np.matmul(phys.Ke[None], d)
+        w = se[act][:, None, None]
+        out += (d * w).reshape(-1, M).T @ Kd.reshape(-1, M)
+    return out

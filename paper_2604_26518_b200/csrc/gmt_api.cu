@@ -212,7 +212,12 @@ int copy_out(gmt_problem p, const LevelBuf& b, float* dst, const float* src, cud
   return GMT_OK;
 }
 
-int set_device(gmt_problem p) {
+// Every public entry point calls this first.  `guess`: the caller is
+// gmt_set_initial_guess, the only call that may still use the event recorded
+// right after the material rebuild's reset (any other call in between may
+// have enqueued work that writes u, so the event is stale then).
+int set_device(gmt_problem p, bool guess = false) {
+  if (!guess) p->u_ready_pending = false;
   CK(cudaSetDevice(p->cfg.device));
   if (p->u0_stale) {
     p->u0_stale = false;
@@ -927,6 +932,11 @@ int slab_levels(int N, int L, int P, int* Ld_out) {
   const int nz0 = N / P;
   int Ld = 0;
   while (Ld < L - 1 && nz0 % (1 << Ld) == 0 && (nz0 >> Ld) >= 2) ++Ld;
+  // the first replicated level Ld is assembled from every slab's region of
+  // nz0 >> Ld planes: that region must be a whole number of planes (an odd
+  // plane count on the last partitioned level would leave coarse planes
+  // unwritten), so step back until nz0 is divisible by 2^Ld
+  while (Ld > 0 && nz0 % (1 << Ld) != 0) --Ld;
   if (Ld < 3) return fail(GMT_ERR_ARG, "slab partition needs >= 3 partitioned levels (res %d, %d slabs)", N, P);
   *Ld_out = Ld;
   return GMT_OK;
@@ -1205,8 +1215,11 @@ int gmt_set_material(gmt_problem p, const void* material, int dtype, int locatio
 
 int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   if (!p) return fail(GMT_ERR_ARG, "null problem");
-  p->u0_stale = false;   // both branches below overwrite every level-0 value
-  TRY(set_device(p));
+  // both branches below overwrite level-0 u at every active node (the host
+  // branch everywhere); stale values at inactive nodes are never read as
+  // data (zero operator rows/columns), so the deferred reset is not needed
+  p->u0_stale = false;
+  TRY(set_device(p, true));
   if (p->grp) return g_set_initial_guess(p->grp, u, location);
   p->refine = false;
   LevelBuf& b = p->lv[0];

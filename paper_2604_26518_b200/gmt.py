@@ -137,11 +137,23 @@ def _buf(a, dtype=None, writable=False):
     raise TypeError(f"unsupported buffer type {type(a)}")
 
 
-def _dptr(a):
+def _dptr(a, size=None):
     p, loc = _buf(a, np.float32)
     if loc != GMT_DEVICE:
         raise ValueError("row-level ops take torch CUDA tensors")
+    _check_size(a, size)
     return p
+
+
+def _numel(a) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _check_size(a, size):
+    """libgmt reads/writes exactly `size` elements through the pointer: a
+    smaller buffer would be overrun, so refuse it here."""
+    if a is not None and size is not None and _numel(a) != size:
+        raise ValueError(f"buffer holds {_numel(a)} elements, expected {size}")
 
 
 def gmt_slab_layout(res: int, levels: int, nslabs: int, rank: int) -> dict:
@@ -251,16 +263,23 @@ class Problem:
         return self.lib.gmt_device_bytes(self._h)
 
     # -- the boundary --------------------------------------------------------
+    def _vsize(self, level: int = 0) -> int:
+        return int(np.prod(self.vec_shape(level)))
+
     def gmt_set_material(self, material):
+        if tuple(material.shape) != (self.nz, self.n, self.n):
+            raise ValueError(f"material must be {(self.nz, self.n, self.n)}, got {tuple(material.shape)}")
         ptr, loc, dt = self._material(material)
         _check(self.lib.gmt_set_material(self._h, ptr, dt, loc), "gmt_set_material")
 
     def gmt_set_initial_guess(self, u=None):
         ptr, loc = _buf(u, np.float32)
+        _check_size(u, self._vsize(0))
         _check(self.lib.gmt_set_initial_guess(self._h, ptr, loc), "gmt_set_initial_guess")
 
     def gmt_inject_correction(self, level: int, e=None):
         ptr, loc = _buf(e, np.float32)
+        _check_size(e, self._vsize(level) if 0 < level < self.levels else None)
         _check(self.lib.gmt_inject_correction(self._h, level, ptr, loc), "gmt_inject_correction")
 
     def gmt_vcycle(self, ncycles: int = 1):
@@ -290,6 +309,7 @@ class Problem:
         if out is None:
             out = np.empty(self.vec_shape(0), dtype=np.float32)
         ptr, loc = _buf(out, np.float32)
+        _check_size(out, self._vsize(0))
         _check(self.lib.gmt_get_solution(self._h, ptr, loc, int(zero_mean)), "gmt_get_solution")
         return out
 
@@ -324,32 +344,38 @@ class Problem:
 
     # -- row-level entry points (torch CUDA tensors) -------------------------
     def gmt_op_apply(self, level, u, y):
-        _check(self.lib.gmt_op_apply(self._h, level, _dptr(u), _dptr(y)), "gmt_op_apply")
+        n = self._vsize(level)
+        _check(self.lib.gmt_op_apply(self._h, level, _dptr(u, n), _dptr(y, n)), "gmt_op_apply")
 
     def gmt_op_residual(self, level, u, f, r):
-        fp = None if f is None else _dptr(f)
-        _check(self.lib.gmt_op_residual(self._h, level, _dptr(u), fp, _dptr(r)), "gmt_op_residual")
+        n = self._vsize(level)
+        fp = None if f is None else _dptr(f, n)
+        _check(self.lib.gmt_op_residual(self._h, level, _dptr(u, n), fp, _dptr(r, n)), "gmt_op_residual")
 
     def gmt_op_jacobi(self, level, u, f, u_out):
-        fp = None if f is None else _dptr(f)
-        _check(self.lib.gmt_op_jacobi(self._h, level, _dptr(u), fp, _dptr(u_out)), "gmt_op_jacobi")
+        n = self._vsize(level)
+        fp = None if f is None else _dptr(f, n)
+        _check(self.lib.gmt_op_jacobi(self._h, level, _dptr(u, n), fp, _dptr(u_out, n)), "gmt_op_jacobi")
 
     def gmt_op_restrict(self, level, r, fc):
-        _check(self.lib.gmt_op_restrict(self._h, level, _dptr(r), _dptr(fc)), "gmt_op_restrict")
+        _check(self.lib.gmt_op_restrict(self._h, level, _dptr(r, self._vsize(level)), _dptr(fc, self._vsize(level + 1))),
+               "gmt_op_restrict")
 
     def gmt_op_prolong_add(self, level, e, u):
-        _check(self.lib.gmt_op_prolong_add(self._h, level, _dptr(e), _dptr(u)), "gmt_op_prolong_add")
+        _check(self.lib.gmt_op_prolong_add(self._h, level, _dptr(e, self._vsize(level + 1)), _dptr(u, self._vsize(level))),
+               "gmt_op_prolong_add")
 
     def gmt_op_loads(self, f):
-        _check(self.lib.gmt_op_loads(self._h, _dptr(f)), "gmt_op_loads")
+        _check(self.lib.gmt_op_loads(self._h, _dptr(f, self._vsize(0))), "gmt_op_loads")
 
     def gmt_op_diagonal(self, level, d):
-        _check(self.lib.gmt_op_diagonal(self._h, level, _dptr(d)), "gmt_op_diagonal")
+        _check(self.lib.gmt_op_diagonal(self._h, level, _dptr(d, self._vsize(level) // self.nrhs)), "gmt_op_diagonal")
 
     def gmt_op_stencil(self, level, S):
-        _check(self.lib.gmt_op_stencil(self._h, level, _dptr(S)), "gmt_op_stencil")
+        _check(self.lib.gmt_op_stencil(self._h, level, _dptr(S, 27 * self.dpn * self._vsize(level) // self.nrhs)),
+               "gmt_op_stencil")
 
     def gmt_op_effective_tensor(self, u):
         CH = (C.c_double * (self.nrhs * self.nrhs))()
-        _check(self.lib.gmt_op_effective_tensor(self._h, _dptr(u), CH), "gmt_op_effective_tensor")
+        _check(self.lib.gmt_op_effective_tensor(self._h, _dptr(u, self._vsize(0)), CH), "gmt_op_effective_tensor")
         return np.array(CH).reshape(self.nrhs, self.nrhs)

@@ -69,6 +69,13 @@ def _cases():
         ("elastic", "truss24", synth.truss(24, "bcc", 0.12), 3),      # ragged vs 32-wide tiles
         ("thermal", "stoch24", synth.stochastic(24, 0.3, seed=2), 3),
         ("elastic", "density16", synth.random_density(16, 1e-3, 1.0, seed=4), 3),
+        # deeper hierarchies: elastic Galerkin levels >= 3 (k_galerkin_elem, the
+        # path the 512^3 bench runs at levels 3-7) down to a 2^3 coarsest grid
+        ("elastic", "gyroid32L5", synth.tpms(32, "gyroid", 0.3), 5),
+        ("thermal", "stoch32L4", synth.stochastic(32, 0.3, seed=5), 4),
+        ("elastic", "truss32L4", synth.truss(32, "octet", 0.07), 4),
+        # BASELINE configs[1]: 64^3 elastic gyroid, 6 load cases, L = 5
+        ("elastic", "gyroid64L5", synth.tpms(64, "gyroid", 0.3), 5),
     ]
 
 
@@ -115,7 +122,7 @@ def _absK(H, l):
     return abs(H.K[l])
 
 
-@pytest.mark.parametrize("level", [0, 1, 2])
+@pytest.mark.parametrize("level", [0, 1, 2, 3, 4])
 def test_apply_residual_jacobi(case, level):
     kind, s, ph, H, P = case
     if level >= H.L:

@@ -243,3 +243,159 @@ def test_gyroid_tensor_sanity():
     assert np.linalg.eigvalsh(CH).min() > -1e-10
     vf = synth.volume_fraction(s)
     assert np.linalg.eigvalsh(vf * ph.C0 - CH).min() > -1e-10
+
+
+# ------------------------------------------------------------------ per-cycle pins (round 2)
+
+def test_jacobi_hand_evaluated_single_voxel_heat():
+    """Sec. 4.6 Eq. 16 update u <- u + omega D^-1 (f - K u), evaluated by hand
+    on the 2^3 periodic grid holding one solid voxel (heat, kappa = 1).
+
+    Every node is then exactly one corner k of that voxel, so K = K_e^th
+    (diagonal 1/3, edge neighbours 0, face and body diagonals -1/12) and
+    D = 1/3 at every node.  Load case m (unit gradient e_m, App. F2):
+    f_k = int dN_k/dx_m = (2 k_m - 1) / 4.
+      sweep 1 from u = 0:  u = omega * 3 * f            -> +-3 omega / 4
+      sweep 2:  K f = f / 2 (K_e applied to the corner coordinate k_m / 2 -
+                1/4: row sums of the -1/12 entries over the k_m = 1 face),
+                u = 3 omega f (2 - 3 omega / 2)          -> +-3 omega / 4 (2 - 1.5 omega)
+    With omega = 0.6: 0.45 and 0.495.  A wrong omega, a diagonal from another
+    operator or an update from the new iterate changes these numbers."""
+    ph = fem.Physics("thermal")
+    s = np.zeros((2, 2, 2), np.float32)
+    s[0, 0, 0] = 1.0
+    H = gmg.Hierarchy(s, ph, 1)
+    assert np.allclose(H.K[0].diagonal(), 1.0 / 3.0)
+    om = 0.6
+    sign = np.zeros((8, 3))
+    for node in range(8):
+        x, y, z = node & 1, (node >> 1) & 1, (node >> 2) & 1
+        sign[node] = [2 * x - 1, 2 * y - 1, 2 * z - 1]
+    u1 = gmg.jacobi(H.K[0], H.Dinv[0], np.zeros((8, 3)), H.f, om, 1)
+    assert np.abs(u1 - sign * 0.45).max() < 1e-15
+    u2 = gmg.jacobi(H.K[0], H.Dinv[0], np.zeros((8, 3)), H.f, om, 2)
+    assert np.abs(u2 - sign * 0.495).max() < 1e-15
+    u3 = gmg.jacobi(H.K[0], H.Dinv[0], u1, H.f, om, 1)          # sweeps compose
+    assert np.abs(u3 - u2).max() < 1e-15
+
+
+def _dense_cycle_operators(H, omega, pre, post, coarse):
+    """Alg. 1 written as matrices instead of a loop.  With S_l = I - omega
+    D_l^-1 K_l, W_l = omega D_l^-1 and Q_l(k) = sum_{j<k} S_l^j W_l (k sweeps
+    from a zero guess), the cycle from a zero guess at level l is
+        B_{L-1} = Q(It_L),
+        B_l     = S_l^post [Q_l(pre) + P_l B_{l+1} P_l^T (I - K_l Q_l(pre))] + Q_l(post),
+    and the level-l cycle from a guess u is u -> E_l u + B_l f with the
+    error propagation E_l = S_l^post (I - P_l B_{l+1} P_l^T K_l) S_l^pre."""
+    L = H.L
+    K = [k.toarray() for k in H.K]
+    P = [p.toarray() for p in H.P]
+    S, Wm = [], []
+    for l in range(L):
+        Wm.append(omega * np.diag(H.Dinv[l]))
+        S.append(np.eye(K[l].shape[0]) - Wm[l] @ K[l])
+
+    def Q(l, k):
+        out = np.zeros_like(K[l])
+        for _ in range(k):
+            out = S[l] @ out + Wm[l]
+        return out
+
+    mp = np.linalg.matrix_power
+    B = [None] * L
+    E = [None] * L
+    B[L - 1] = Q(L - 1, coarse)
+    E[L - 1] = mp(S[L - 1], coarse)
+    for l in range(L - 2, -1, -1):
+        Qp = Q(l, pre)
+        I = np.eye(K[l].shape[0])
+        C = P[l] @ B[l + 1] @ P[l].T
+        B[l] = mp(S[l], post) @ (Qp + C @ (I - K[l] @ Qp)) + Q(l, post)
+        E[l] = mp(S[l], post) @ (I - C @ K[l]) @ mp(S[l], pre)
+    return E, B, S, P
+
+
+@pytest.mark.parametrize("kind,n,L,pre,post,coarse", [("thermal", 8, 3, 2, 2, 5),
+                                                      ("elastic", 4, 2, 1, 3, 4),
+                                                      ("thermal", 8, 2, 3, 1, 7)])
+def test_vcycle_equals_dense_error_propagation(kind, n, L, pre, post, coarse):
+    """gmg.vcycle (the loop of Alg. 1) == E_0 u + B_0 f from the matrix
+    recursion above, for random u and f.  Dropping post-smoothing,
+    restricting before pre-smoothing, a wrong sweep count or a wrong level's
+    diagonal all change E_0 or B_0."""
+    ph = fem.Physics(kind)
+    om = 0.45 if kind == "elastic" else 0.6
+    s = synth.random_occupancy(n, 0.6, seed=3)
+    H = gmg.Hierarchy(s, ph, L)
+    E, B, _, _ = _dense_cycle_operators(H, om, pre, post, coarse)
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal(H.f.shape)
+    f = rng.standard_normal(H.f.shape)
+    got = gmg.vcycle(H, u, f1=f, omega=om, pre=pre, post=post, coarse=coarse)
+    want = E[0] @ u + B[0] @ f
+    assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
+
+
+def test_alg2_injection_equals_dense_coarse_error_propagation():
+    """Alg. 2 line 6: the level-1 cycle starts from the injected e_hat instead
+    of 0, so vcycle(.., inject={1: e}) - vcycle(..) = S_0^post P_0 E_1 e."""
+    ph = fem.Physics("thermal")
+    s = synth.random_occupancy(8, 0.6, seed=4)
+    H = gmg.Hierarchy(s, ph, 3)
+    om, pre, post, coarse = 0.6, 2, 2, 4
+    E, B, S, P = _dense_cycle_operators(H, om, pre, post, coarse)
+    rng = np.random.default_rng(2)
+    e = rng.standard_normal((H.K[1].shape[0], 3))
+    f = rng.standard_normal(H.f.shape)
+    a = gmg.vcycle(H, np.zeros_like(f), f1=f, omega=om, pre=pre, post=post, coarse=coarse, inject={1: e})
+    b = gmg.vcycle(H, np.zeros_like(f), f1=f, omega=om, pre=pre, post=post, coarse=coarse)
+    want = np.linalg.matrix_power(S[0], post) @ P[0] @ E[1] @ e
+    assert np.abs((a - b) - want).max() <= 1e-11 * np.abs(want).max()
+
+
+def test_project_zero_mean_worked_example():
+    """Sec. 4.5 gauge sum_i u_i = 0 over active nodes, per component and load
+    case; inactive nodes are left alone.  Worked by hand: active values
+    (1, 2, 6) have mean 3."""
+    u = np.array([[1.0], [2.0], [5.0], [6.0]])
+    act = np.array([True, True, False, True])
+    got = gmg.project_zero_mean(u, 1, act)
+    assert np.array_equal(got, np.array([[-2.0], [-1.0], [5.0], [3.0]]))
+    # dpn = 2, two load cases: components are separate, constants vanish
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((5, 2, 2))
+    v -= v.mean(axis=0, keepdims=True)                   # zero mean per (component, case)
+    shift = np.array([[3.0, -1.0], [0.5, 7.0]])          # [component, case]
+    u = (v + shift[None]).reshape(10, 2)
+    got = gmg.project_zero_mean(u, 2)
+    assert np.abs(got - v.reshape(10, 2)).max() < 1e-14
+
+
+def test_relative_residual_closed_form():
+    """Sec. 5.2 r = ||f - K u||_2 / ||f||_2 per load case; a zero right-hand
+    side reports the absolute norm (hand values)."""
+    import scipy.sparse as sp
+    K = sp.identity(4, format="csr") * 2.0
+    u = np.ones((4, 2))
+    f = np.zeros((4, 2))
+    f[:, 0] = 3.0                        # r = 1 everywhere: ||r|| = 2, ||f|| = 6
+    got = fem.relative_residual(K, u, f)
+    assert abs(got[0] - 1.0 / 3.0) < 1e-15
+    assert abs(got[1] - 4.0) < 1e-15     # f = 0: ||-2 * 1|| = 4
+
+
+@pytest.mark.parametrize("kind", ["elastic", "thermal"])
+def test_effective_tensor_planes_partition(kind):
+    """Plane-restricted App. F1/F2 sums over a partition of the planes add up
+    to effective_tensor * N^3 (the definition split over a partition of the
+    elements), on a random field and a density material."""
+    ph = fem.Physics(kind)
+    n = 8
+    s = synth.random_density(n, 0.0, 1.0, seed=6)
+    s[s < 0.3] = 0.0
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal((n ** 3 * ph.dpn, ph.nrhs))
+    want = fem.effective_tensor(s, ph, u) * n ** 3
+    un = fem.to_node_layout(u, n, ph.dpn)                      # [z, y, x, m, c]
+    got = sum(fem.effective_tensor_planes(s, ph, lambda z: un[z], a, b) for a, b in ((0, 3), (3, 4), (4, 8)))
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
