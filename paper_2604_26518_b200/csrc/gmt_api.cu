@@ -21,7 +21,8 @@
 
 #include "../../include/gmt.h"
 #include "gmt_fem.h"
-#include "k_fine_tiled.cuh"
+#include "k_coarse_tiled.cuh"
+#include "k_l0.cuh"
 #include "k_level.cuh"
 #include "k_reduce.cuh"
 #include "k_setup.cuh"
@@ -98,6 +99,12 @@ Geo geo(int n, int nz) {
   return g;
 }
 
+// k_active_sum: node columns of geo(), planes strided over at most 8 z-blocks
+dim3 zsum_grid(const LevelBuf& b) {
+  const Geo g = geo(b.n, b.nz);
+  return dim3(g.grid.x, g.grid.y, std::min(b.nz, 8));
+}
+
 struct Group;   // slab partition (gmt_group.inc)
 
 }  // namespace
@@ -142,7 +149,7 @@ struct gmt_problem_s {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int tntx = 0, tnty = 0;
-  int variant = 0;            // level-0 tiled kernel: 0 scalar (3 load cases/CTA), 1 packed f32x2 pairs
+  L0Consts l0c{};             // level-0 sweep constants (k_l0)
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
@@ -291,6 +298,19 @@ int ch_grid() {
   return g;
 }
 
+// Level-0 sweep geometry (k_l0): 32 x 8 node columns, 32-plane chunks, one
+// CTA per load-case group.
+template <int DPN>
+dim3 l0_grid(gmt_problem p) {
+  const LevelBuf& b = p->lv[0];
+  constexpr int NG = Tr<DPN>::NR / L0V<DPN>::NRG;
+  return dim3((b.n + L0_X - 1) / L0_X, (b.n + L0_Y - 1) / L0_Y, ((b.nz + L0_ZC - 1) / L0_ZC) * NG);
+}
+template <int DPN>
+constexpr size_t l0_smem() {
+  return (size_t)L0_NB * (L0V<DPN>::NRG * DPN * L0_PLS + L0_CPL) * sizeof(float);
+}
+
 template <int DPN>
 int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part,
               int skip_void = 0) {
@@ -301,92 +321,25 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = b.cs;
   if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
-    // explicit right-hand side f (iterative refinement) only in the default kernels
-    int var = f ? 0 : p->variant;
-    if (p->variant == 5) var = b.n % TX_X == 0 ? 5 : 0;   // x-pairs (n % 64 == 0) also take an explicit rhs
-    const bool packed = DPN == 3 && var == 1, pairs = DPN == 3 && (var == 2 || var == 4);
-    const bool zb = var == 3 || var == 4, x2 = var == 5;
-    const int NRG = DPN == 3 ? (packed || pairs ? 2 : 3) : 3, NG = Tr<DPN>::NR / NRG;
+    // the V-cycle's level-0 sweep: uniform + interface nodes in one launch
     const ZMap z = p->zm(0);
-    const dim3 grid(x2 ? b.n / TX_X : p->tntx, p->tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * NG), block(TT_X, TT_Y);
-    const size_t shm = x2 ? (size_t)TT_NB * NRG * DPN * TX_PLS * sizeof(float)
-                          : (size_t)(zb ? TT_NB2 : TT_NB) * NRG * DPN * TT_PLS * sizeof(float);
-    const int nbt = grid.x * grid.y * grid.z;
-    double* part_i = part ? part + (size_t)nbt * 2 * Tr<DPN>::NR : nullptr;
-    const int nbi = (p->icount + 127) / 128;
-    if (packed) {
+    const dim3 grid = l0_grid<DPN>(p), block(L0_X, L0_TY);
+    const size_t shm = l0_smem<DPN>();
+    const float* s0 = p->s;
+    if (f) {
       if (mode == M_JACOBI)
-        k_fine_tiled2<M_JACOBI><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
-                                                          p->tntx, p->tnty);
+        k_l0<DPN, M_JACOBI, true><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
+                                                             p->tflag, p->tntx, p->tnty, f);
       else
-        k_fine_tiled2<M_RESID><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag,
-                                                         p->tntx, p->tnty);
-    } else if (x2) {
-      if (mode == M_JACOBI)
-        k_fine_tiled_x2<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                    cs, p->tflag, p->tntx, p->tnty, f);
-      else
-        k_fine_tiled_x2<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                   cs, p->tflag, p->tntx, p->tnty, f);
-    } else if (zb) {
-      if (pairs) {
-        if (mode == M_JACOBI)
-          k_fine_tiled_zb<3, M_JACOBI, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                    cs, p->tflag, p->tntx, p->tnty);
-        else
-          k_fine_tiled_zb<3, M_RESID, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                   cs, p->tflag, p->tntx, p->tnty);
-      } else {
-        if (mode == M_JACOBI)
-          k_fine_tiled_zb<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc,
-                                                                      part, cs, p->tflag, p->tntx, p->tnty);
-        else
-          k_fine_tiled_zb<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc,
-                                                                     part, cs, p->tflag, p->tntx, p->tnty);
-      }
-    } else if (pairs) {
-      if (mode == M_JACOBI)
-        k_fine_tiled<3, M_JACOBI, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                               p->tflag, p->tntx, p->tnty);
-      else
-        k_fine_tiled<3, M_RESID, 2><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs,
-                                                              p->tflag, p->tntx, p->tnty);
+        k_l0<DPN, M_RESID, true><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
+                                                            p->tflag, p->tntx, p->tnty, f);
     } else {
-      if (f) {
-        if (mode == M_JACOBI)
-          k_fine_tiled<DPN, M_JACOBI, 3, false, true><<<grid, block, shm, st>>>(
-              p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag, p->tntx, p->tnty, f);
-        else
-          k_fine_tiled<DPN, M_RESID, 3, false, true><<<grid, block, shm, st>>>(
-              p->code, z, u, z, out, b.n, b.nz, p->fc, part, cs, p->tflag, p->tntx, p->tnty, f);
-      } else {
-        if (mode == M_JACOBI)
-          k_fine_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                     cs, p->tflag, p->tntx, p->tnty);
-        else
-          k_fine_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(p->code, z, u, z, out, b.n, b.nz, p->fc, part,
-                                                                    cs, p->tflag, p->tntx, p->tnty);
-      }
-    }
-    LAUNCHED(p);
-    if (nbi > 0) {
-      if (f) {
-        if (mode == M_JACOBI)
-          k_iface<DPN, M_JACOBI, true><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs,
-                                                            p->ilist, p->icount, f);
-        else
-          k_iface<DPN, M_RESID, true><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs,
-                                                           p->ilist, p->icount, f);
-      } else {
-        if (mode == M_JACOBI)
-          k_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
-                                                      p->icount);
-        else
-          k_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(p->s, z, u, z, out, b.n, b.nz, p->fc, part_i, cs, p->ilist,
-                                                     p->icount);
-      }
-    } else {
-      return GMT_OK;
+      if (mode == M_JACOBI)
+        k_l0<DPN, M_JACOBI, false><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
+                                                              p->tflag, p->tntx, p->tnty, nullptr);
+      else
+        k_l0<DPN, M_RESID, false><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
+                                                             p->tflag, p->tntx, p->tnty, nullptr);
     }
   } else if (l == 0) {
     const ZMap z = p->zm(0);
@@ -403,11 +356,11 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     const dim3 grid(b.tntx, b.tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * (Tr<DPN>::NR / 3)), block(TT_X, TT_Y);
     const size_t shm = (size_t)TT_NB * 3 * DPN * TT_PLS * sizeof(float);
     if (mode == M_JACOBI)
-      k_fine_tiled<DPN, M_JACOBI, 3, true><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, p->fc, nullptr,
-                                                                     cs, b.tflag, b.tntx, b.tnty, f, p->hc[l]);
+      k_coarse_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, om, cs, b.tflag,
+                                                                 b.tntx, b.tnty, f, p->hc[l]);
     else
-      k_fine_tiled<DPN, M_RESID, 3, true><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, p->fc, nullptr,
-                                                                    cs, b.tflag, b.tntx, b.tnty, f, p->hc[l]);
+      k_coarse_tiled<DPN, M_RESID, 3><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, om, cs, b.tflag,
+                                                                b.tntx, b.tnty, f, p->hc[l]);
     LAUNCHED(p);
     if (b.icount == 0) return GMT_OK;
     const int nbi = (b.icount + 127) / 128;
@@ -726,16 +679,11 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
   return GMT_OK;
 }
 
-// Number of fp64 partial rows the level-0 residual launch writes (tiled CTAs,
-// then interface blocks); fexp: explicit right-hand side (default kernels).
+// Number of fp64 partial rows the level-0 residual launch writes (one per CTA).
 template <int DPN>
-int l0_partials(gmt_problem p, bool fexp) {
-  const LevelBuf& b = p->lv[0];
-  int v = fexp ? 0 : p->variant;
-  if (p->variant == 5) v = b.n % TX_X == 0 ? 5 : 0;
-  const int ng = DPN == 3 ? (v == 1 || v == 2 || v == 4 ? 3 : 2) : 1;
-  const int gx = v == 5 ? b.n / TX_X : p->tntx;
-  return gx * p->tnty * ((b.nz + TT_ZC - 1) / TT_ZC) * ng + (p->icount + 127) / 128;
+int l0_partials(gmt_problem p, bool /*fexp*/) {
+  const dim3 g = l0_grid<DPN>(p);
+  return (int)(g.x * g.y * g.z);
 }
 
 template <int DPN>
@@ -828,10 +776,10 @@ int zero_mean(gmt_problem p, float* dst) {
   constexpr int V = Tr<DPN>::V;
   const LevelBuf& b = p->lv[0];
   const Geo g = geo(b.n, b.nz);
-  k_active_sum<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->part,
-                                                        (ptrdiff_t)b.nodes);
+  const dim3 gs = zsum_grid(b);
+  k_active_sum<DPN><<<gs, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->part, (ptrdiff_t)b.nodes);
   LAUNCHED(p);
-  TRY(reduce_launch(p, g.nblk, V + 1));
+  TRY(reduce_launch(p, (int)(gs.x * gs.y * gs.z), V + 1));
   k_sub_mean<DPN><<<g.grid, g.block, 0, p->stream>>>(p->s, p->zm(0), dst, b.n, b.nz, p->red,
                                                       (ptrdiff_t)b.nodes);
   LAUNCHED(p);
@@ -988,6 +936,23 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     const double hpp = p->ed.H[13 * 9 + dq * p->ed.dpn + dq];   // ElementData::H is [d][9]
     p->fc.wd[q] = (float)(cfg.omega / hpp);
   }
+  {
+    L0Tables t;
+    if (!build_l0_tables(p->ed, cfg.omega, &t)) {
+      delete p;
+      return fail(GMT_ERR_ARG, "level-0 stencil factorisation / element symmetry check failed");
+    }
+    p->l0c.k1 = (float)t.k1;
+    p->l0c.k2 = (float)t.k2;
+    p->l0c.k3 = (float)t.k3;
+    p->l0c.omega = (float)cfg.omega;
+    for (int i = 0; i < 3; ++i) {
+      p->l0c.wd[i] = (float)t.wd[i];
+      p->l0c.kdiag[i] = (float)t.kdiag[i];
+    }
+    for (int i = 0; i < 72; ++i) p->l0c.K0[i] = (float)t.K0[i];
+    for (int i = 0; i < 18; ++i) p->l0c.F0[i] = (float)t.F0[i];
+  }
   std::vector<float> m1(8 * nd * nd);
   for (int j = 0; j < 8; ++j)
     for (int i = 0; i < nd * nd; ++i) m1[j * nd * nd + i] = (float)p->ed.M1[j][i];
@@ -1020,7 +985,6 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   // coarse levels at least this fine use the tiled sweep (env override for tests)
   int coarse_tiled_min = 64;
   if (const char* v = getenv("GMT_COARSE_TILED_MIN")) coarse_tiled_min = std::max(2, atoi(v));
-  size_t max_blk = 0;
   for (int l = 0; l < L; ++l) {
     LevelBuf& b = p->lv[l];
     b.n = cfg.res >> l;
@@ -1068,9 +1032,18 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         return bail(fail(GMT_ERR_CUDA, "memset failed"));
       b.tflag += tfp * TF_GLO;
     }
-    max_blk = std::max(max_blk, (size_t)geo(b.n, b.nz).nblk);
   }
-  p->part_cap = (2 * max_blk + p->lv[0].nodes / 128 + 1) * 32 + (size_t)RED_BLOCKS * 64;
+  {
+    // partial rows: level-0 sweep CTAs x 2 NR, the C^H grid x NQ, the gauge
+    // sums x (V + 1); then the reduction stage area
+    const int nr = p->nr, nq = nr * (nr + 1) / 2;
+    const dim3 g0 = p->dpn == 3 ? l0_grid<3>(p) : l0_grid<1>(p);
+    const dim3 gz = zsum_grid(p->lv[0]);
+    const size_t chg = (size_t)(p->dpn == 3 ? ch_grid<3>() : ch_grid<1>());
+    size_t rows = std::max((size_t)g0.x * g0.y * g0.z * 2 * nr, chg * nq);
+    rows = std::max(rows, (size_t)gz.x * gz.y * gz.z * (V + 1));
+    p->part_cap = rows + (size_t)RED_BLOCKS * 64;
+  }
   if ((rc = dalloc(p, (void**)&p->part, p->part_cap * sizeof(double)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->red, 64 * sizeof(double)))) return bail(rc);
   const size_t pl0 = (size_t)p->N * p->N;
@@ -1103,37 +1076,21 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     if ((rc = dalloc(p, &p->cub_tmp, bytes))) return bail(rc);
   }
   {
-    if (const char* v = getenv("GMT_TILED_VARIANT")) p->variant = atoi(v);
-    const int shm2 = TT_NB * 6 * TT_PLS * (int)sizeof(float);
     const int shm3 = TT_NB * 9 * TT_PLS * (int)sizeof(float);
     const int shm1 = TT_NB * 3 * TT_PLS * (int)sizeof(float);
-    const int shm3z = TT_NB2 * 9 * TT_PLS * (int)sizeof(float), shm2z = TT_NB2 * 6 * TT_PLS * (int)sizeof(float);
-    const int shm1z = TT_NB2 * 3 * TT_PLS * (int)sizeof(float);
-    const int shm3x = TT_NB * 9 * TX_PLS * (int)sizeof(float), shm1x = TT_NB * 3 * TX_PLS * (int)sizeof(float);
-    if (cudaFuncSetAttribute(k_fine_tiled2<M_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
-        cudaFuncSetAttribute(k_fine_tiled2<M_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_JACOBI, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<3, M_RESID, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_JACOBI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<3, M_RESID, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm2z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z) ||
-        cudaFuncSetAttribute(k_fine_tiled_zb<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1z) ||
-        cudaFuncSetAttribute(k_fine_tiled_x2<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3x) ||
-        cudaFuncSetAttribute(k_fine_tiled_x2<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3x) ||
-        cudaFuncSetAttribute(k_fine_tiled_x2<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1x) ||
-        cudaFuncSetAttribute(k_fine_tiled_x2<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1x))
+    const int l3 = (int)l0_smem<3>(), l1 = (int)l0_smem<1>();
+    if (cudaFuncSetAttribute(k_coarse_tiled<3, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_coarse_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
+        cudaFuncSetAttribute(k_coarse_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_coarse_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
+        cudaFuncSetAttribute(k_l0<3, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
+        cudaFuncSetAttribute(k_l0<3, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
+        cudaFuncSetAttribute(k_l0<3, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
+        cudaFuncSetAttribute(k_l0<3, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
+        cudaFuncSetAttribute(k_l0<1, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
+        cudaFuncSetAttribute(k_l0<1, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
+        cudaFuncSetAttribute(k_l0<1, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
+        cudaFuncSetAttribute(k_l0<1, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1))
       return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
   }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);

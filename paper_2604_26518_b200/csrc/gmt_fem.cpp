@@ -231,4 +231,111 @@ void homogeneous_levels(const ElementData& ed, int levels, double (*Khom)[24 * 2
     }
 }
 
+
+namespace {
+
+// The kernel's uniform-node arithmetic (k_l0.cuh) on one staged plane at z
+// offset c from the target, in double: v[q][b+1][a+1] are the in-plane values
+// of component q; returns the contribution to (H v)_p for each p.
+void l0_uniform_emulate(int dpn, double k1, double k2, double k3, const double v[3][3][3], int c, double out[3]) {
+  double Ym[3] = {0, 0, 0}, Yd[3] = {0, 0, 0}, Yg[3] = {0, 0, 0};
+  for (int q = 0; q < dpn; ++q) {
+    double Mx[3], ND[3], G[3];
+    for (int r = 0; r < 3; ++r) {
+      const double vm = v[q][r][0], v0 = v[q][r][1], vp = v[q][r][2];
+      const double S = vm + vp;
+      Mx[r] = 4 * v0 + S;
+      ND[r] = -2 * v0 + S;
+      G[r] = vp - vm;
+    }
+    const double Ms = Mx[0] + Mx[2];
+    const double mm36 = 4 * Mx[1] + Ms, nmd6 = -2 * Mx[1] + Ms, ndm6 = 4 * ND[1] + ND[0] + ND[2];
+    const double gg = G[2] - G[0], gm6 = 4 * G[1] + G[0] + G[2], mg6 = Mx[2] - Mx[0];
+    if (dpn == 1) {
+      Ym[0] = -k1 * (ndm6 + nmd6);
+      Yd[0] = k1 * mm36;
+    } else if (q == 0) {
+      Ym[0] += -k2 * nmd6 - k1 * ndm6;
+      Yd[0] = k2 * mm36;
+      Ym[1] += k3 * gg;
+      Yg[2] += k3 * gm6;
+    } else if (q == 1) {
+      Ym[1] += -k1 * nmd6 - k2 * ndm6;
+      Yd[1] = k2 * mm36;
+      Ym[0] += k3 * gg;
+      Yg[2] += k3 * mg6;
+    } else {
+      Ym[2] = -k2 * (ndm6 + nmd6);
+      Yd[2] = k1 * mm36;
+      Yg[0] = k3 * gm6;
+      Yg[1] = k3 * mg6;
+    }
+  }
+  for (int p = 0; p < dpn; ++p) {
+    if (c == 1) out[p] = Ym[p] - Yd[p] + Yg[p];        // plane above the target
+    else if (c == 0) out[p] = 4 * Ym[p] + 2 * Yd[p];
+    else out[p] = Ym[p] - Yd[p] - Yg[p];
+  }
+}
+
+}  // namespace
+
+bool build_l0_tables(const ElementData& ed, double omega, L0Tables* t) {
+  const int dpn = ed.dpn, nd = ed.nd, nr = ed.nrhs;
+  *t = L0Tables{};
+  if (dpn == 3) {
+    t->k1 = (ed.lam + 2 * ed.mu) / 36.0;
+    t->k2 = ed.mu / 36.0;
+    t->k3 = -(ed.lam + ed.mu) / 24.0;
+  } else {
+    t->k1 = ed.lam / 36.0;   // kappa
+  }
+  double kmax = 0.0, fmax = 0.0, hmax = 0.0;
+  for (int i = 0; i < nd * nd; ++i) kmax = std::fmax(kmax, std::fabs(ed.K[i]));
+  for (int i = 0; i < nd * nr; ++i) fmax = std::fmax(fmax, std::fabs(ed.F[i]));
+  for (int i = 0; i < 27 * 9; ++i) hmax = std::fmax(hmax, std::fabs(ed.H[i]));
+  // sum-factorised uniform stencil vs H, offset by offset
+  for (int d = 0; d < 27; ++d) {
+    const int a = d % 3 - 1, b = (d / 3) % 3 - 1, c = d / 9 - 1;
+    for (int q = 0; q < dpn; ++q) {
+      double v[3][3][3] = {};
+      v[q][b + 1][a + 1] = 1.0;
+      double out[3] = {0, 0, 0};
+      l0_uniform_emulate(dpn, t->k1, t->k2, t->k3, v, c, out);
+      for (int p = 0; p < dpn; ++p)
+        if (std::fabs(out[p] - ed.H[d * 9 + p * dpn + q]) > 1e-12 * hmax) return false;
+    }
+  }
+  for (int p = 0; p < dpn; ++p) {
+    const double hpp = ed.H[13 * 9 + p * dpn + p];
+    if (!(hpp > 0)) return false;
+    t->wd[p] = omega / hpp;
+    t->kdiag[p] = ed.K[p * nd + p];
+    for (int k = 0; k < 8; ++k)
+      for (int q = 0; q < dpn; ++q) t->K0[(p * 8 + k) * dpn + q] = ed.K[p * nd + k * dpn + q];
+    for (int m = 0; m < nr; ++m) t->F0[p * nr + m] = ed.F[p * nr + m];
+  }
+  // reflection symmetry: corner c's rows from corner 0's (t_r = -1 where c_r = 1)
+  for (int ci = 0; ci < 8; ++ci) {
+    const double tr[3] = {(ci & 1) ? -1.0 : 1.0, (ci & 2) ? -1.0 : 1.0, (ci & 4) ? -1.0 : 1.0};
+    for (int p = 0; p < dpn; ++p) {
+      const double sp = dpn == 3 ? tr[p] : 1.0;
+      if (std::fabs(ed.K[(ci * dpn + p) * nd + ci * dpn + p] - t->kdiag[p]) > 1e-13 * kmax) return false;
+      for (int cj = 0; cj < 8; ++cj)
+        for (int q = 0; q < dpn; ++q) {
+          const double sq = dpn == 3 ? tr[q] : 1.0;
+          const double want = sp * sq * t->K0[(p * 8 + (ci ^ cj)) * dpn + q];
+          if (std::fabs(ed.K[(ci * dpn + p) * nd + cj * dpn + q] - want) > 1e-13 * kmax) return false;
+        }
+      for (int m = 0; m < nr; ++m) {
+        double tau;
+        if (dpn == 1) tau = tr[m];
+        else tau = m < 3 ? 1.0 : (m == 3 ? tr[1] * tr[2] : (m == 4 ? tr[0] * tr[2] : tr[0] * tr[1]));
+        if (std::fabs(ed.F[(ci * dpn + p) * nr + m] - sp * tau * t->F0[p * nr + m]) > 1e-13 * fmax) return false;
+      }
+    }
+  }
+  return true;
+}
+
 }  // namespace gmt

@@ -36,4 +36,22 @@ bool build_element_data(int physics, double E, double nu, double kappa, ElementD
 // used for the material-independent unit tables (lam, mu) = (1,0), (0,1).
 bool build_element_data_lm(int physics, double lam, double mu, double kappa, ElementData* out);
 
+// Constants of the level-0 sweep (k_l0.cuh, L0Consts) in double precision,
+// derived from an ElementData and checked against it:
+//   * k1, k2, k3: the sum-factorised homogeneous stencil; the kernel's exact
+//     sequence of in-plane filters and z weights is replayed on unit impulses
+//     and must reproduce H (all 27 offsets, all blocks);
+//   * K0 / F0: the corner-0 rows of K_e and f_e; every corner's rows must
+//     follow from them by the reflection symmetry of the cube element
+//     K_e[(c,p),(c^k,q)] = t_p t_q K0[p][k][q], f_e[(c,p),m] = t_p tau_m f0[p][m].
+// Returns false (and the problem is not created) if any check fails.
+struct L0Tables {
+  double k1, k2, k3;
+  double wd[3];
+  double K0[72];
+  double F0[18];
+  double kdiag[3];
+};
+bool build_l0_tables(const ElementData& ed, double omega, L0Tables* out);
+
 }  // namespace gmt

@@ -61,55 +61,6 @@ __device__ __forceinline__ void node_uniform(const Get& get, float c, float lam,
   for (int k = 0; k < V; ++k) acc[k] *= c;
 }
 
-// node_uniform for elasticity with two load cases (m = 0, 1 of the group)
-// processed as packed FP32 pairs: one FADD2 / FFMA2 per component pair.  The
-// operands come from two scalar shared-memory loads each (planar staging);
-// the combined coefficients (h, h) are loop invariants.  Same arithmetic,
-// same rounding as node_uniform.
-template <class Get>
-__device__ __forceinline__ void node_uniform_pk(const Get& get, float c, float lam, float mu, const float (&ui)[6],
-                                                float (&acc)[6], float (&D)[3]) {
-#pragma unroll
-  for (int p = 0; p < 3; ++p) {
-    const int i = 13 * 9 + p * 3 + p;
-    D[p] = c * fmaf(lam, CT<3>::Hl(i), mu * CT<3>::Hm(i));
-  }
-  // two accumulator sets (even / odd offsets): 6 independent FFMA2 chains
-  f2 u2[3], a2[3], b2[3];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    u2[q] = pk2(ui[q], ui[3 + q]);
-    a2[q] = 0ull;
-    b2[q] = 0ull;
-  }
-#pragma unroll
-  for (int d = 14; d < 27; ++d) {
-    const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
-    f2 w[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const f2 pp = pk2(get(dx, dy, dz, q), get(dx, dy, dz, 3 + q));
-      const f2 mm = pk2(get(-dx, -dy, -dz, q), get(-dx, -dy, -dz, 3 + q));
-      w[q] = add2(sub2(pp, u2[q]), sub2(mm, u2[q]));
-    }
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (!hom_nz(d, p, q)) continue;
-        const int i = d * 9 + p * 3 + q;
-        const float h = fmaf(lam, CT<3>::Hl(i), mu * CT<3>::Hm(i));
-        if (d & 1) b2[p] = fma2(pk2(h, h), w[q], b2[p]);
-        else a2[p] = fma2(pk2(h, h), w[q], a2[p]);
-      }
-  }
-#pragma unroll
-  for (int p = 0; p < 3; ++p) a2[p] = add2(a2[p], b2[p]);
-  const f2 c2 = pk2(c, c);
-#pragma unroll
-  for (int p = 0; p < 3; ++p) upk2(mul2(a2[p], c2), acc[p], acc[3 + p]);
-}
-
 // Interface node: A(d) = sum_{e shared} s_e K_e[corner_e(i), corner_e(i+d)]
 // formed in registers (lam- and mu-parts), applied in difference form
 // K u = sum_{d != 0} A(d) (u_{i+d} - u_i); blocks whose elements are void for

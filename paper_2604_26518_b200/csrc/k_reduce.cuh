@@ -35,160 +35,14 @@ k_reduce_stage(const double* __restrict__ part, int nblk, int nv, double* __rest
 //   Q_mn += s_e (x_0^m - u_e^m)^T K_e (x_0^n - u_e^n),  n >= m.
 // K_e = sum_g w_g B_g^T C_0 B_g exactly (2x2x2 Gauss, App. F1 "K_e = int B^T
 // C_0 B"), and B_g x_0^m = e_m (the unit strain), so each term is
-//   sum_g w_g (e_m - eps_g(u^m)) : C_0 : (e_n - eps_g(u^n)).
-// Gradients come from nodal differences along the element edges (exact in fp32
-// even when |u| ~ N): d u / d x_r is constant along r and bilinear in the two
-// transverse coordinates, so its 8 Gauss values are a separable 2x2
-// interpolation of the 4 r-edge differences.  The Gauss points are processed
-// as (z-half, y) rows of two points (x = G0, G1) held as packed FP32 pairs
-// (FADD2/FFMA2/FMUL2): d/dx is equal in both, d/dy and d/dz differ.  The
-// strains of all load cases of a half are staged in shared memory
-// (thread-fastest float2, conflict-free) for the NR(NR+1)/2 Gram sums;
-// isotropic C_0 gives sigma = lam tr(eps) I + 2 mu eps (thermal: q = kappa
-// grad, lam carries kappa).  Grid-stride over the active-element list;
-// per-element fp32 sums are accumulated in fp64 per thread, then one block
-// partial of the upper triangle.
+//   sum_g w_g (e_m - eps_g(u^m)) : C_0 : (e_n - eps_g(u^n)),
+// evaluated in the Walsh basis of the Gauss rule:
 constexpr int CH_THREADS = 64;
 #ifndef GMT_CH_UNROLL
 #define GMT_CH_UNROLL 2
 #endif
 constexpr int CH_UNROLL = GMT_CH_UNROLL;   // load cases staged per step (gathers in flight)
 
-// Kept for A/B (build with -DGMT_CH_GAUSS); the default is the Walsh form below.
-template <int DPN>
-__global__ void __launch_bounds__(CH_THREADS, 6)
-k_effective_tensor_gauss(const float* __restrict__ s, const float* __restrict__ u, ZMap zu, int n, int nz,
-                         float lam, float mu, double* __restrict__ part, ptrdiff_t cs,
-                         const int* __restrict__ elist, int ecount) {
-  using T = Tr<DPN>;
-  constexpr int NR = T::NR;
-  constexpr int NQ = NR * (NR + 1) / 2;
-  constexpr int NE = DPN == 3 ? 6 : 3;
-  constexpr float G0 = 0.21132486540518713f;  // (1 - 1/sqrt(3)) / 2
-  constexpr float G1 = 0.78867513459481287f;  // (1 + 1/sqrt(3)) / 2
-  const ptrdiff_t plane = (ptrdiff_t)n * n;
-  // e_m - eps(u^m) at the Gauss pair (gy, x = G0|G1) of the current z-half
-  __shared__ f2 Esh[NR * 2 * NE][CH_THREADS];
-  const f2 Gp = pk2(G0, G1);
-  const f2 two_mu = pk2(2.f * mu, 2.f * mu), lam2 = pk2(lam, lam), mu2 = pk2(mu, mu);
-  double q[NQ];
-#pragma unroll
-  for (int k = 0; k < NQ; ++k) q[k] = 0.0;
-  // work item = (element, z-half): adjacent lanes take the two halves of one
-  // element, so each corner gather serves both from the same sectors
-  const long long items = 2ll * ecount;
-  for (long long ii = blockIdx.x * (long long)blockDim.x + threadIdx.x; ii < items;
-       ii += (long long)gridDim.x * blockDim.x) {
-    const int it = (int)(ii >> 1), h = (int)(ii & 1);
-    const ptrdiff_t eid = __ldg(elist + it);
-    const float se = __ldg(s + eid);
-    const int x = (int)(eid % n), y = (int)((eid / n) % n), z = (int)(eid / plane);
-    unsigned off[8];   // within one component plane (< 2^32 floats)
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      off[k] = (unsigned)((ptrdiff_t)zu(z + (k >> 2)) * plane + (ptrdiff_t)wrapi(y + ((k >> 1) & 1), n) * n +
-                          wrapi(x + (k & 1), n));
-    f2 qf[NQ];
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) qf[k] = 0ull;
-    {
-      const float gz = h ? G1 : G0;
-#pragma unroll 3
-      for (int m = 0; m < NR; ++m) {
-        f2 gxv[2][DPN], gyv[DPN], gzv[2][DPN];   // [gy][c] pairs over x = G0, G1
-#pragma unroll
-        for (int c = 0; c < DPN; ++c) {
-          const float* bp = u + (ptrdiff_t)(m * DPN + c) * cs;
-          float uc[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) uc[k] = __ldg(bp + off[k]);
-          float ax[2], ay[2];
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {   // x-edges (y = j), interpolated to z = gz
-            const float d0 = uc[1 + 2 * j] - uc[2 * j], d1 = uc[5 + 2 * j] - uc[4 + 2 * j];
-            ax[j] = fmaf(gz, d1 - d0, d0);
-          }
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {   // y-edges (x = i), interpolated to z = gz
-            const float d0 = uc[2 + i] - uc[i], d1 = uc[6 + i] - uc[4 + i];
-            ay[i] = fmaf(gz, d1 - d0, d0);
-          }
-          const float tx = ax[1] - ax[0];
-          gxv[0][c] = pk2(fmaf(G0, tx, ax[0]), fmaf(G0, tx, ax[0]));
-          gxv[1][c] = pk2(fmaf(G1, tx, ax[0]), fmaf(G1, tx, ax[0]));
-          gyv[c] = fma2(Gp, pk2(ay[1] - ay[0], ay[1] - ay[0]), pk2(ay[0], ay[0]));
-          // z-edges (x = i, y = j): pairs over x, then y = gy
-          const f2 dxy0 = sub2(pk2(uc[5] - uc[1], uc[5] - uc[1]), pk2(uc[4] - uc[0], uc[4] - uc[0]));
-          const f2 dxy1 = sub2(pk2(uc[7] - uc[3], uc[7] - uc[3]), pk2(uc[6] - uc[2], uc[6] - uc[2]));
-          const f2 a0 = fma2(Gp, dxy0, pk2(uc[4] - uc[0], uc[4] - uc[0]));   // y = 0 edge pair at x = G0, G1
-          const f2 a1 = fma2(Gp, dxy1, pk2(uc[6] - uc[2], uc[6] - uc[2]));   // y = 1
-          const f2 da = sub2(a1, a0);
-          gzv[0][c] = fma2(pk2(G0, G0), da, a0);
-          gzv[1][c] = fma2(pk2(G1, G1), da, a0);
-        }
-#pragma unroll
-        for (int gy = 0; gy < 2; ++gy) {
-          f2 E[NE];
-          if constexpr (DPN == 3) {   // Voigt (11,22,33,23,13,12), engineering shear
-            E[0] = sub2(pk2(m == 0 ? 1.f : 0.f, m == 0 ? 1.f : 0.f), gxv[gy][0]);
-            E[1] = sub2(pk2(m == 1 ? 1.f : 0.f, m == 1 ? 1.f : 0.f), gyv[1]);
-            E[2] = sub2(pk2(m == 2 ? 1.f : 0.f, m == 2 ? 1.f : 0.f), gzv[gy][2]);
-            E[3] = sub2(pk2(m == 3 ? 1.f : 0.f, m == 3 ? 1.f : 0.f), add2(gzv[gy][1], gyv[2]));
-            E[4] = sub2(pk2(m == 4 ? 1.f : 0.f, m == 4 ? 1.f : 0.f), add2(gzv[gy][0], gxv[gy][2]));
-            E[5] = sub2(pk2(m == 5 ? 1.f : 0.f, m == 5 ? 1.f : 0.f), add2(gyv[0], gxv[gy][1]));
-          } else {
-            E[0] = sub2(pk2(m == 0 ? 1.f : 0.f, m == 0 ? 1.f : 0.f), gxv[gy][0]);
-            E[1] = sub2(pk2(m == 1 ? 1.f : 0.f, m == 1 ? 1.f : 0.f), gyv[0]);
-            E[2] = sub2(pk2(m == 2 ? 1.f : 0.f, m == 2 ? 1.f : 0.f), gzv[gy][0]);
-          }
-#pragma unroll
-          for (int i = 0; i < NE; ++i) Esh[(m * 2 + gy) * NE + i][threadIdx.x] = E[i];
-        }
-      }
-#pragma unroll 1
-      for (int gy = 0; gy < 2; ++gy) {
-        f2 E[NR][NE];
-#pragma unroll
-        for (int m = 0; m < NR; ++m)
-#pragma unroll
-          for (int i = 0; i < NE; ++i) E[m][i] = Esh[(m * 2 + gy) * NE + i][threadIdx.x];
-        int qi = 0;
-#pragma unroll
-        for (int m = 0; m < NR; ++m) {
-          f2 sg[NE];
-          if constexpr (DPN == 3) {
-            const f2 tr = add2(add2(E[m][0], E[m][1]), E[m][2]);
-            const f2 lt = mul2(lam2, tr);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) sg[i] = fma2(two_mu, E[m][i], lt);
-#pragma unroll
-            for (int i = 3; i < 6; ++i) sg[i] = mul2(mu2, E[m][i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) sg[i] = mul2(lam2, E[m][i]);
-          }
-#pragma unroll
-          for (int nn = m; nn < NR; ++nn) {
-            f2 a = qf[qi];
-#pragma unroll
-            for (int i = 0; i < NE; ++i) a = fma2(sg[i], E[nn][i], a);
-            qf[qi++] = a;
-          }
-        }
-      }
-    }
-    const double w = 0.125 * (double)se;
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      float a, b;
-      upk2(qf[k], a, b);
-      q[k] = fma(w, (double)(a + b), q[k]);
-    }
-  }
-  block_reduce_store<NQ>(q, part + (ptrdiff_t)blockIdx.x * NQ);
-}
-
-// Same App. F1/F2 sums in the Walsh basis of the 2x2x2 Gauss rule (default).
 // With centred signs s_r = +-1 of the Gauss coordinates, every strain
 // component of a trilinear element is a combination of the 8 Walsh functions
 // {1, s_x, s_y, s_z, s_x s_y, s_x s_z, s_y s_z, s_x s_y s_z}, which are
@@ -414,13 +268,8 @@ k_effective_tensor(const float* __restrict__ s, const float* __restrict__ u, ZMa
   block_reduce_store<NQ, CH_THREADS / 32>(q, part + (ptrdiff_t)blockIdx.x * NQ);
 }
 
-#ifdef GMT_CH_GAUSS
-#define GMT_CH_KERNEL k_effective_tensor_gauss
-#define GMT_CH_ITEMS 2
-#else
 #define GMT_CH_KERNEL k_effective_tensor
 #define GMT_CH_ITEMS 1
-#endif
 
 // Iterative refinement: (hi, lo) += e on active level-0 nodes (code != 0;
 // e is zero elsewhere).  Error-free two-sum of hi + e, the rounding error
@@ -455,13 +304,13 @@ k_active_sum(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, 
   constexpr int V = Tr<DPN>::V;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int z = blockIdx.z;
   const bool valid = (x < n) && (y < n);
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   double a[V + 1];
 #pragma unroll
   for (int k = 0; k <= V; ++k) a[k] = 0.0;
-  if (valid) {
+  // planes blockIdx.z, blockIdx.z + gridDim.z, ... (fixed order: deterministic)
+  for (int z = blockIdx.z; valid && z < nz; z += gridDim.z) {
     bool act = false;
     const int xs0 = wrapi(x - 1, n), ys0 = wrapi(y - 1, n), zs0 = zs(z - 1);
 #pragma unroll
@@ -471,8 +320,8 @@ k_active_sum(const float* __restrict__ s, ZMap zs, const float* __restrict__ u, 
     if (act) {
       const float* p = u + (z * plane + (ptrdiff_t)y * n + x);
 #pragma unroll
-      for (int k = 0; k < V; ++k) a[k] = p[k * cs];
-      a[V] = 1.0;
+      for (int k = 0; k < V; ++k) a[k] += p[k * cs];
+      a[V] += 1.0;
     }
   }
   const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);

@@ -75,3 +75,8 @@ def test_slab_layout_errors_and_geometry():
         gmt.gmt_slab_layout(16, 3, 4, 0)      # 4 planes per slab: only 2 partitioned levels
     with pytest.raises(GmtError):
         gmt.gmt_slab_layout(30, 2, 4, 0)      # not divisible
+    # 12 planes per slab: level 2 would hold 3 planes per slab and the first
+    # replicated level 1.5 -- rejected instead of silently leaving planes unwritten
+    with pytest.raises(GmtError):
+        gmt.gmt_slab_layout(48, 4, 4, 0)
+    assert gmt.gmt_slab_layout(48, 4, 2, 1) == {"z0": 24, "nz": 24, "Ld": 3, "L": 4}

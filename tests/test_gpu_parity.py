@@ -354,3 +354,30 @@ def test_material_reset_and_initial_guess(kind):
     P.gmt_set_material(np.ascontiguousarray(s, dtype=np.float32))
     P.gmt_vcycle(1)
     assert np.array_equal(P.gmt_get_solution(), a)
+
+
+def test_level0_vcycle_kernel_one_sweep(case):
+    """The V-cycle's level-0 kernel itself (k_l0: uniform nodes sum-factorised,
+    interface nodes from the staged planes): with one level and one coarsest
+    sweep, gmt_vcycle is exactly one damped-Jacobi sweep (Sec. 4.6 Eq. 16),
+    compared element by element with the oracle at every active node; then
+    its residual mode through gmt_residual_norms (Sec. 5.2) on the same u."""
+    kind, s, ph, H, _ = case
+    n = s.shape[0]
+    rng = np.random.default_rng(21)
+    act = H.active[0]
+    u = rng.standard_normal(H.f.shape) * act[:, None] + 0.3 * n * np.sin(np.arange(H.f.shape[0]))[:, None] * act[:, None]
+    want = gmg.jacobi(H.K[0], H.Dinv[0], u, H.f, OMEGA[kind], 1)
+    with _problem(s, kind, 1, coarse_sweeps=1) as P1:
+        P1.gmt_set_initial_guess(np.ascontiguousarray(to_gpu(u, n, ph.dpn), dtype=np.float32))
+        r_g, ar_g, af_g = P1.gmt_residual_norms()
+        P1.gmt_vcycle(1)
+        got = from_gpu(P1.gmt_get_solution())
+    uf = from_gpu(to_gpu(u, n, ph.dpn).astype(np.float32))       # the fp32 input the GPU saw
+    want = gmg.jacobi(H.K[0], H.Dinv[0], uf, H.f, OMEGA[kind], 1)
+    sc = (abs(H.K[0]) @ np.abs(uf) + np.abs(H.f)) * H.Dinv[0][:, None] * OMEGA[kind] + np.abs(uf)
+    a2 = np.repeat(act[:, None], ph.nrhs, axis=1)
+    err = np.abs(got - want)[a2]
+    assert np.all(err <= 1e-5 * sc[a2] + 1e-30), f"max ratio {(err / (1e-5 * sc[a2])).max():.2f}"
+    r_o = fem.relative_residual(H.K[0], uf, H.f)
+    assert np.allclose(r_g, r_o, rtol=1e-4), (r_g, r_o)

@@ -45,6 +45,9 @@ CASES = [
     ("thermal", "stoch32-P2", lambda: synth.stochastic(32, 0.3, seed=5), 4, 2),
     ("elastic", "octet64-P4", lambda: synth.truss(64, "octet", 0.08), 5, 4),
     ("thermal", "density32-P4", lambda: synth.random_density(32, 1e-3, 1.0, seed=6), 4, 4),
+    # non-power-of-2 slab: 24 planes per slab, levels 0-2 partitioned, the
+    # replicated level 3 assembled from 3-plane regions
+    ("elastic", "gyroid48-P2", lambda: synth.tpms(48, "gyroid", 0.3), 4, 2),
 ]
 
 
