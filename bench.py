@@ -1,17 +1,22 @@
 """bench.py -- GMG V-cycle throughput of libgmt on B200 (driver contract).
 
-Metric (BASELINE.json): "512^3 elasticity GMG V-cycles/s & DOF/s at 1/2/4/8 B200;
-% HBM roofline".  Workload at N=1: configs[4]'s problem -- 512^3 linear
-elasticity on a gyroid TPMS lattice, all 6 load cases, one V-cycle from a
-given initial guess -- which fits one B200 (configs[1] 64^3 is a parity
-case).  One step = one pass of the whole hot path:
-  Galerkin coarse-operator build from the (device-resident) material
-  + set the given initial guess (Alg. 2 line 1)
+Metric (BASELINE.json "512^3 elasticity GMG V-cycles/s & DOF/s at 1/2/4/8
+B200; % HBM roofline"), reported as throughput of the homogenisation step in
+active DOF-load-cases per second: one step = one pass of the whole hot path
+ on the 512^3 gyroid TPMS (configs[4]'s problem, which
+fits one B200; configs[1] 64^3 is a parity case):
+    Galerkin coarse-operator build from the (device-resident) material
+  + the given initial guess (Alg. 2 line 1)
   + one V-cycle (damped-Jacobi smoothing, residual, restriction,
     prolongation, coarse levels, coarsest solve) for all 6 load cases
   + C^H reduction (App. F1) read back to the host.
-value = steps/s ("V-cycles/s" as single-cycle homogenisations per second);
-DOF/s = 3 N^3 * 6 load cases * value.
+value = DPN * (active nodes) * NRHS / step time.  V-cycles/s (= steps/s) and
+the V-cycle time on its own are separate keys.  Both arms print the same
+metric, unit and config; the reference arm is the FP64 oracle (there is no
+reference implementation to install) timed on the host cores on a bounded
+sample of the same workload (the 64^3 cell of the same generator, whose
+throughput in the same unit it reports); our arm adds a like-for-like GPU
+line at that sample size.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--res 512] [--physics elastic]
   python bench.py --impl reference ...   (the FP64 oracle on host cores)
@@ -21,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -31,12 +37,86 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_L0_JACOBI = {"elastic": 2 * 18 * 4 + 4, "thermal": 2 * 3 * 4 + 4}  # per active node, DESIGN.md Sec. 8(d)
+SAMPLE_N = 64   # the reference arm's bounded sample: configs[1]'s size (~10 s of oracle work per step)
+
+
+def physics_dims(physics: str):
+    return (3, 6) if physics == "elastic" else (1, 3)   # (DPN, NRHS)
+
+
+def metric_name(args) -> str:
+    return (f"{args.res}^3 {args.physics} GMG homogenisation throughput: active DOF x load case x V-cycle "
+            f"per second (step = Galerkin build + 1 V-cycle + C^H)")
+
+
+def workload_config(args) -> dict:
+    dpn, nr = physics_dims(args.physics)
+    return {"workload": f"{args.res}^3 {args.physics} {args.geometry} v_f={args.vf}, {nr} load cases, "
+                        f"one V-cycle from a given initial guess + C^H",
+            "smoother": "damped Jacobi (2 pre, 2 post, 16 coarsest sweeps)",
+            "l2": "inputs larger than L2 (level-0 vectors 9.7 GB at 512^3)"}
+
+
+# --------------------------------------------------------------------------- activity model
+
+def level_activity(s: np.ndarray, levels: int):
+    """Per level l: (n_l, active nodes, interface nodes) of the homogeneity
+    pyramid: level-l elements carry the common scale of their
+    2^l x 2^l x 2^l voxels (or -1 if mixed); a node is active if one of its 8
+    incident elements is non-void and an interface node if they differ."""
+    out = []
+    e = s.astype(np.float32)
+    for l in range(levels):
+        n = e.shape[0]
+        if l > 0:
+            v = e.reshape(n // 2, 2, n // 2, 2, n // 2, 2).transpose(0, 2, 4, 1, 3, 5).reshape(n // 2, n // 2, n // 2, 8)
+            same = np.all(v == v[..., :1], axis=-1)
+            e = np.where(same, v[..., 0], np.float32(-1))
+            n //= 2
+        # node (z, y, x) has incident elements (z-1..z, y-1..y, x-1..x)
+        nz_any = np.zeros(e.shape, bool)
+        mixed = e < 0
+        for dz in (0, 1):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    r = np.roll(e, shift=(dz, dy, dx), axis=(0, 1, 2))
+                    nz_any |= r != 0
+                    mixed |= (r != e) | (r < 0)
+        out.append((n, int(nz_any.sum()), int((nz_any & mixed).sum())))
+    return out
+
+
+def vcycle_bytes(act, dpn: int, nr: int, pre=2, post=2, coarse=16) -> tuple[float, float]:
+    """Algorithmic HBM bytes of one V-cycle, every level:
+    per active node and sweep read u, write u (4V each), read f (levels >= 1,
+    4V) and the node code (4 B); interface nodes of coarse levels also read
+    their 27-point stencil (27 DPN^2 x 4 B); the residual pass as a sweep;
+    restriction reads the fine residual and writes the coarse rhs; the coarse
+    error is zeroed; prolongation reads the coarse error and updates the fine
+    solution.  Returns (total, level-0 share)."""
+    V = 4 * dpn * nr
+    L = len(act)
+    tot = 0.0
+    lvl0 = 0.0
+    for l, (n, A, I) in enumerate(act):
+        f_read = V if l > 0 else 0
+        sweep = (2 * V + f_read + 4) * A + (27 * dpn * dpn * 4 * I if l > 0 else 0)
+        if l == L - 1:
+            b = coarse * sweep
+        else:
+            A1 = act[l + 1][1]
+            b = (pre + post + 1) * sweep                      # smoothing + residual
+            b += V * A + V * A1                               # restriction
+            b += V * A1                                       # zero coarse error
+            b += V * A1 + 2 * V * A + 4 * A                   # prolongation + correction
+        tot += b
+        if l == 0:
+            lvl0 = b
+    return tot, lvl0
 
 
 def active_nodes(s: np.ndarray, z0: int = 0, nz: int | None = None) -> int:
-    """Nodes of planes [z0, z0+nz) touching at least one non-void voxel (the
-    sparse active set)."""
+    """Nodes of planes [z0, z0+nz) touching at least one non-void voxel."""
     n = s.shape[0]
     nz = n - z0 if nz is None else nz
     occ = np.take(s != 0, np.arange(z0 - 1, z0 + nz) % n, axis=0)
@@ -60,25 +140,25 @@ def parse():
     ap.add_argument("--vf", type=float, default=0.3)
     ap.add_argument("--levels", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-like", action="store_true", help="skip the like-for-like GPU line at the sample size")
     ap.add_argument("--breakdown", action="store_true", help="extra pass with per-class event timing")
     ap.add_argument("--no-solve", action="store_true", help="skip the (untimed) full solve to 1e-5")
     return ap.parse_args()
 
 
-def make_material(args):
+def make_material(geometry: str, n: int, vf: float):
     import synth
-    n = args.res
-    if args.geometry == "gyroid":
-        return synth.tpms(n, "gyroid", args.vf)
-    if args.geometry == "gyroid_sheet":
-        return synth.tpms(n, "gyroid", args.vf, sheet=True)
-    if args.geometry == "truss":
+    if geometry == "gyroid":
+        return synth.tpms(n, "gyroid", vf)
+    if geometry == "gyroid_sheet":
+        return synth.tpms(n, "gyroid", vf, sheet=True)
+    if geometry == "truss":
         return synth.truss(n, "octet", 0.05)
-    if args.geometry == "stochastic":
-        return synth.stochastic(n, args.vf, seed=0)
-    if args.geometry == "solid":
+    if geometry == "stochastic":
+        return synth.stochastic(n, vf, seed=0)
+    if geometry == "solid":
         return synth.solid(n)
-    raise ValueError(args.geometry)
+    raise ValueError(geometry)
 
 
 class Clocks:
@@ -141,9 +221,9 @@ def measured_peaks():
 
 def ncu_traffic(args, world: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the roofline
-    kernel from the committed `ncu --set full` capture (profiles/r1/traffic.json),
+    kernel from the committed `ncu --set full` capture (profiles/r2/traffic.json),
     when it was taken on this exact single-GPU workload; else None."""
-    p = os.path.join(ROOT, "profiles", "r1", "traffic.json")
+    p = os.path.join(ROOT, "profiles", "r2", "traffic.json")
     if world != 1 or not os.path.exists(p):
         return None, None
     with open(p) as fh:
@@ -155,71 +235,129 @@ def ncu_traffic(args, world: int):
 
 # --------------------------------------------------------------------------- oracle leg
 
-ORACLE_SAMPLE_N = 64   # configs[1]'s size: ~8 s of single-thread oracle work
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max([int(d.get("num_threads", 1)) for d in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count() or 1
 
 
-def oracle_sample(physics: str, n_sample: int = ORACLE_SAMPLE_N, vf: float = 0.3):
-    """One step of the same workload run by the FP64 oracle on a bounded
-    sample (an n_sample^3 gyroid, same generator and settings), single
-    threaded.  Returns (seconds, sample description)."""
-    from threadpoolctl import threadpool_limits
-
-    import synth
+def oracle_step(physics: str, geometry: str, n: int, vf: float):
+    """One step of the workload run by the FP64 oracle at resolution n (same
+    generator and settings): assembly + Galerkin hierarchy, one V-cycle from
+    zero, C^H.  Returns (seconds, active DOF-load-cases)."""
     from oracle import fem, gmg
-    s = synth.tpms(n_sample, "gyroid", vf)
+    s = make_material(geometry, n, vf)
     ph = fem.Physics(physics)
     om = 0.45 if physics == "elastic" else 0.6
-    L = gmg.default_levels(n_sample)
-    with threadpool_limits(1):
-        t0 = time.perf_counter()
-        H = gmg.Hierarchy(s, ph, L)                     # assembly + Galerkin build
-        u0 = np.zeros_like(H.f)
-        u = gmg.vcycle(H, u0, omega=om, pre=2, post=2, coarse=16)
-        fem.effective_tensor(s, ph, u)
-        dt = time.perf_counter() - t0
-    return dt, f"{n_sample}^3 gyroid v_f={vf}, L={L}: assembly+Galerkin+1 V-cycle+C^H, 1 thread"
+    L = gmg.default_levels(n)
+    t0 = time.perf_counter()
+    H = gmg.Hierarchy(s, ph, L)
+    u = gmg.vcycle(H, np.zeros_like(H.f), omega=om, pre=2, post=2, coarse=16)
+    fem.effective_tensor(s, ph, u)
+    dt = time.perf_counter() - t0
+    return dt, int(H.active[0].sum()) * ph.nrhs
 
 
-def cpu_baseline(args):
-    n_s = ORACLE_SAMPLE_N
-    dt, desc = oracle_sample(args.physics, n_s, args.vf)
-    scale = (args.res / n_s) ** 3          # oracle cost is linear in the node count
-    return {"value": 1.0 / (dt * scale), "unit": "V-cycles/s", "cores": 1, "kind": "oracle",
-            "sample": desc + f"; {dt:.2f} s, scaled by (N/{n_s})^3 = {scale:.0f} to the {args.res}^3 workload"}
+def sample_desc(args, n, L_note=""):
+    return (f"{n}^3 cell of the same workload ({args.geometry}, v_f={args.vf}, {args.physics}): "
+            f"assembly + Galerkin hierarchy + 1 V-cycle + C^H by the FP64 oracle (scipy.sparse kernels "
+            f"single-threaded, numpy BLAS on {blas_threads()} threads){L_note}")
+
+
+def cpu_baseline(args, reps: int = 1):
+    ts, dofs = [], 0
+    for _ in range(reps):
+        dt, dofs = oracle_step(args.physics, args.geometry, SAMPLE_N, args.vf)
+        ts.append(dt)
+    dt = float(np.mean(ts))
+    return {"value": dofs / dt, "unit": "DOF/s", "cores": blas_threads(), "kind": "oracle",
+            "sample": sample_desc(args, SAMPLE_N) + f"; {dt:.2f} s per step, mean of {reps}"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = []
-    n_s = ORACLE_SAMPLE_N
     for _ in range(args.warmup):
-        oracle_sample(args.physics, n_s, args.vf)
+        oracle_step(args.physics, args.geometry, SAMPLE_N, args.vf)
+    ts, dofs = [], 0
     for _ in range(args.steps):
-        dt, desc = oracle_sample(args.physics, n_s, args.vf)
-        steps.append(dt)
-    scale = (args.res / n_s) ** 3
-    ms = float(np.mean(steps)) * scale * 1e3
-    val = 1e3 / ms
-    out = {"impl": "reference", "metric": "512^3 elasticity GMG V-cycles/s (single-cycle homogenisation)",
-           "value": val, "unit": "V-cycles/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-           "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{args.res}^3 {args.physics} gyroid TPMS v_f={args.vf}, 6 load cases"},
-           "cpu_baseline": {"value": val, "unit": "V-cycles/s", "cores": 1, "kind": "oracle",
-                            "sample": desc + f"; per-step time scaled by (N/{n_s})^3={scale:.0f}"},
-           "e2e": {"value": val, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        dt, dofs = oracle_step(args.physics, args.geometry, SAMPLE_N, args.vf)
+        ts.append(dt)
+    ms = float(np.mean(ts)) * 1e3
+    val = dofs / (ms * 1e-3)
+    out = {"impl": "reference", "metric": metric_name(args), "value": val, "unit": "DOF/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(args), "sample_res": SAMPLE_N,
+           "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": blas_threads(), "kind": "oracle",
+                            "sample": sample_desc(args, SAMPLE_N) + f"; {ms:.0f} ms per step"},
+           "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
 
 # --------------------------------------------------------------------------- our leg
+
+def maybe_spawn(args):
+    """--gpus N without a torchrun environment: re-launch as N ranks."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+
+
+def time_steps(fn, steps, stream, sync):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+    sync()
+    return e0.elapsed_time(e1) / steps
+
+
+def like_for_like(args, steps: int, warmup: int):
+    """The same step on the GPU at the reference arm's sample size."""
+    import torch
+    from paper_2604_26518_b200 import Problem
+    s = make_material(args.geometry, SAMPLE_N, args.vf)
+    dpn, nr = physics_dims(args.physics)
+    import synth
+    u0 = torch.from_numpy(synth.initial_guess(SAMPLE_N, nr, dpn, seed=1, material=s)).cuda()
+    s_dev = torch.from_numpy(np.ascontiguousarray(s)).cuda()
+    with Problem(s_dev, physics=args.physics, levels=0) as P:
+        st = torch.cuda.ExternalStream(P.stream)
+
+        def step():
+            P.gmt_set_material(s_dev)
+            P.gmt_set_initial_guess(u0)
+            P.gmt_vcycle(1)
+            return P.gmt_homogenize()
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        ms = time_steps(step, steps, st, torch.cuda.synchronize)
+    dofs = dpn * active_nodes(s) * nr
+    return {"res": SAMPLE_N, "value": dofs / (ms * 1e-3), "unit": "DOF/s", "ms_per_step": ms,
+            "note": "same step on the GPU at the reference arm's sample size"}
+
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    maybe_spawn(args)
     import torch
 
     import synth
@@ -228,8 +366,6 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        world = max(world, 1)
     dist = world > 1
     if dist:
         import torch.distributed as td
@@ -237,9 +373,9 @@ def main():
     torch.cuda.set_device(local)
     build.build()
 
-    s = make_material(args)
+    s = make_material(args.geometry, args.res, args.vf)
     n = args.res
-    nr, dpn = (6, 3) if args.physics == "elastic" else (3, 1)
+    dpn, nr = physics_dims(args.physics)
     if dist:
         # one z-slab per rank (gmt_create_dist): halos by ncclSend/Recv,
         # replicated coarse levels by ncclAllGather, dot products by ncclAllReduce
@@ -258,7 +394,7 @@ def main():
         P = Problem(s_dev, physics=args.physics, levels=args.levels, device=local, dist=(rank, world, nid))
     else:
         P = Problem(s_dev, physics=args.physics, levels=args.levels, device=local)
-    P.gmt_profile_enable(1)   # bracket the dominant kernel (level-0 Jacobi) live
+    P.gmt_profile_enable(1)   # bracket the dominant kernel (level-0 Jacobi sweep) live
     st = torch.cuda.ExternalStream(P.stream)
 
     def step():
@@ -271,64 +407,68 @@ def main():
         step()
     P.gmt_profile_collect()
     P.gmt_profile_read(0, reset=True)
-    rel_before = None
 
     clocks = Clocks(local)
     if dist:
         td.barrier()
     torch.cuda.synchronize()
     launches0 = P.gmt_kernel_launches()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     clocks.start()
-    with torch.cuda.stream(st):
-        e0.record(st)
-        for _ in range(args.steps):
-            CH = step()
-            P.gmt_profile_collect()
-        e1.record(st)
-    torch.cuda.synchronize()
+    out_CH = [None]
+
+    def timed_step():
+        out_CH[0] = step()
+        P.gmt_profile_collect()
+
+    ms = time_steps(timed_step, args.steps, st, torch.cuda.synchronize)
     clk = clocks.stop()
+    CH = out_CH[0]
     if dist:
         td.barrier()
     launches = P.gmt_kernel_launches() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
     if dist:
-        t = torch.tensor([ms], device="cuda")
-        td.all_reduce(t, op=td.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = gd.max_over_ranks(ms, device="cuda")
     k_ms, k_cnt = P.gmt_profile_read(0)
     rel, _, _ = P.gmt_residual_norms()
 
-    # ---- e2e: public API with host buffers: the step's inputs (u8 occupancy
-    # and the given initial guess, both in pinned host memory) are copied to
-    # the device inside the timed region every step, C^H is read back.
-    s_u8 = torch.from_numpy((s_loc > 0).astype(np.uint8)).pin_memory().numpy()
-    if not np.all((s_loc == 0) | (s_loc == 1)):
-        s_u8 = None
-    s_host = np.ascontiguousarray(s_loc) if s_u8 is None else s_u8
-    u0_host = u0_dev.cpu().pin_memory().numpy()
-
-    def e2e_step():
-        P.gmt_set_material(s_host)
-        P.gmt_set_initial_guess(u0_host)
-        P.gmt_vcycle(1)
-        return P.gmt_homogenize()
-
-    for _ in range(2):
-        e2e_step()
+    # the V-cycle alone (same state as a step: material built, guess set)
+    P.gmt_set_material(s_dev)
+    P.gmt_set_initial_guess(u0_dev)
+    P.gmt_vcycle(1)
     torch.cuda.synchronize()
     if dist:
         td.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    vc_ms = time_steps(lambda: P.gmt_vcycle(1), args.steps, st, torch.cuda.synchronize)
     if dist:
-        e2e_ms = gd.max_over_ranks(e2e_ms, device="cuda")
-    u0_bytes = int(u0_host.nbytes)
-    del u0_host
+        vc_ms = gd.max_over_ranks(vc_ms, device="cuda")
+
+    # ---- e2e through the public API with host buffers: the u8 occupancy and
+    # the given initial guess on the active nodes (compact layout, Sec. 4.1.1)
+    # come from pinned host memory every step, C^H goes back to the host.
+    binary = bool(np.all((s_loc == 0) | (s_loc == 1)))
+    s_host = torch.from_numpy((s_loc > 0).astype(np.uint8) if binary else s_loc).pin_memory().numpy()
+    e2e = None
+    if not dist:
+        P.gmt_set_material(s_dev)
+        P.gmt_set_initial_guess(u0_dev)
+        uc_host = torch.from_numpy(P.gmt_get_solution_compact()).pin_memory().numpy()
+
+        def e2e_step():
+            P.gmt_set_material(s_host)
+            P.gmt_set_initial_guess_compact(uc_host)
+            P.gmt_vcycle(1)
+            return P.gmt_homogenize()
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        e2e = {"ms_per_step": e2e_ms, "h2d": int(s_host.nbytes + uc_host.nbytes)}
+        del uc_host
 
     # north star's second half: full GMG solve to 1e-5 relative residual from
     # a zero initial guess (informational, outside the timed steps)
@@ -371,7 +511,7 @@ def main():
     levels = P.levels
     P.close()
     n_act = active_nodes(s, z0, nz)
-    bytes_launch = BYTES_L0_JACOBI[args.physics] * n_act
+    bytes_launch = (2 * 4 * dpn * nr + 4) * n_act      # level-0 sweep: read u, write u, node code
     avg_ms = k_ms / max(k_cnt, 1)
     if dist:   # aggregate over ranks: all bytes / slowest rank's launch
         tb = torch.tensor([float(bytes_launch), float(n_act), float(launches)], dtype=torch.float64, device="cuda")
@@ -383,42 +523,52 @@ def main():
     if rank != 0:
         return
 
-    nodes = n ** 3
     hbm, hbm_src = measured_peaks()
-    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     hbm_agg = hbm * world
+    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     traffic, traffic_src = ncu_traffic(args, world)
-    value = 1e3 / ms
-    dofs = dpn * nodes * nr
+    act = level_activity(s, levels)
+    vb, vb0 = vcycle_bytes(act, dpn, nr)
+    dofs = dpn * n_act * nr
+    value = dofs / (ms * 1e-3)
     out = {
-        "metric": "512^3 elasticity GMG V-cycles/s (single-cycle homogenisation: Galerkin build + 1 V-cycle + C^H)",
-        "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": metric_name(args),
+        "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{n}^3 {args.physics} {args.geometry} TPMS v_f={args.vf}, {nr} load cases, "
-                               f"one V-cycle from a given initial guess",
-                   "levels": levels, "smoother": "damped Jacobi (2 pre, 2 post, 16 coarsest)",
-                   "l2": "inputs larger than L2 (9.7 GB level-0 vectors)",
+        "config": {**workload_config(args), "levels": levels,
                    "parallelism": f"slab{world} (z-slabs, NCCL halos)" if dist else "single GPU"},
-        "dof_per_s": dofs * value,
-        "roofline": {"bound": "hbm", "kernel": "level-0 damped-Jacobi sweep (k_fine_tiled + k_iface)",
+        "vcycles_per_s": 1e3 / ms, "vcycle_ms": vc_ms, "active_nodes": n_act, "active_dof_x_cases": dofs,
+        "roofline": {"bound": "hbm", "kernel": "level-0 damped-Jacobi sweep (k_l0)",
                      "achieved": achieved, "peak": hbm_agg, "unit": "GB/s", "frac": achieved / hbm_agg,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
-                     "bytes_per_launch": bytes_launch, "bytes_rule": "148 B (elastic) x active nodes",
-                     "active_nodes": n_act, "avg_launch_ms": avg_ms, "launches_timed": k_cnt,
-                     "share_of_step": k_ms / args.steps / ms},
+                     "bytes_per_launch": bytes_launch,
+                     "bytes_rule": f"(2 x 4 x {dpn * nr} + 4) B x active nodes (read u, write u, node code)",
+                     "avg_launch_ms": avg_ms, "launches_timed": k_cnt, "share_of_step": k_ms / args.steps / ms},
+        "roofline_vcycle": {"bound": "hbm", "achieved": vb / (vc_ms * 1e-3) / 1e9, "peak": hbm_agg, "unit": "GB/s",
+                            "frac": vb / (vc_ms * 1e-3) / 1e9 / hbm_agg, "bytes_per_vcycle": vb,
+                            "level0_bytes": vb0, "vcycle_ms": vc_ms,
+                            "levels": [{"n": a[0], "active": a[1], "interface": a[2]} for a in act],
+                            "rule": "bench.vcycle_bytes (DESIGN.md Sec. 8(d))"},
         "clocks": clk,
         "gpu_launches": int(launches),
-        "e2e": {"value": 1e3 / e2e_ms, "unit": "V-cycles/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(s_host.nbytes + u0_bytes), "d2h_bytes_per_step": nr * nr * 8,
-                "note": "pinned host material (uint8 occupancy) + pinned host initial guess through "
-                        "gmt_set_material/gmt_set_initial_guess/gmt_vcycle/gmt_homogenize"},
         "residual_after_cycle": float(np.max(rel)),
         "solve": solve,
         "C_H_diag": [float(CH[i, i]) for i in range(nr)],
     }
+    if e2e:
+        out["e2e"] = {"value": dofs / (e2e["ms_per_step"] * 1e-3), "unit": "DOF/s", "ms_per_step": e2e["ms_per_step"],
+                      "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": nr * nr * 8,
+                      "note": "pinned host u8 occupancy (gmt_set_material) + pinned host initial guess on the "
+                              "active nodes (gmt_set_initial_guess_compact) + gmt_vcycle + C^H to host "
+                              "(gmt_homogenize), wall clock"}
+    else:
+        out["e2e"] = {"value": None, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                      "note": "not measured for slab-partitioned runs"}
     if breakdown:
         out["breakdown"] = breakdown
+    if not dist and not args.no_like:
+        out["like_for_like"] = like_for_like(args, max(args.steps, 5), max(args.warmup, 3))
     if not args.no_cpu_baseline and not dist:
         out["cpu_baseline"] = cpu_baseline(args)
     print(json.dumps(out))

@@ -169,6 +169,23 @@ GMT_API int gmt_homogenize(gmt_problem p, double* CH);
  * the active nodes (to the copy only).  Synchronises when location==GMT_HOST. */
 GMT_API int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean);
 
+/* Compact active-node I/O (Sec. 4.1.1 "sparse voxels": the paper's input and
+ * network output live on the active nodes only).  The active set of the
+ * current material is the sorted list of level-0 nodes i = x + n (y + n z)
+ * touching a nonzero voxel; a compact vector holds NRHS * DPN * A floats,
+ * layout [m][c][k] (k = position in the list, k fastest).
+ *   gmt_active_count: A (>= 0), or a negative GMT_ERR_* code.
+ *   gmt_active_nodes: writes the A node indices (int32) to `nodes`.
+ *   gmt_set_initial_guess_compact: Alg. 2 line 1 from a compact vector (the
+ *     same semantics as gmt_set_initial_guess, a fraction of the bytes).
+ *   gmt_get_solution_compact: the finest-level solution at the active nodes
+ *     (zero_mean as in gmt_get_solution).  Synchronises for GMT_HOST.
+ * Single-device problems only (GMT_ERR_STATE on slab-partitioned ones). */
+GMT_API long long gmt_active_count(gmt_problem p);
+GMT_API int gmt_active_nodes(gmt_problem p, int32_t* nodes, int location);
+GMT_API int gmt_set_initial_guess_compact(gmt_problem p, const float* u_active, int location);
+GMT_API int gmt_get_solution_compact(gmt_problem p, float* u_active, int location, int zero_mean);
+
 /* Problem properties. */
 GMT_API int gmt_num_levels(gmt_problem p);
 GMT_API int gmt_level_res(gmt_problem p, int level);      /* n_l */

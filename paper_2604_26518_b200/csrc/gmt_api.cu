@@ -139,13 +139,14 @@ struct gmt_problem_s {
   uint8_t* tflag = nullptr;   // level-0 tile activity flags (k_tile_flags)
   uint8_t* iflag = nullptr;   // level-0 interface-node flags (k_material_scan)
   float* code = nullptr;      // level-0 node class: uniform voxel scale, or -1 (interface)
-  int* ilist = nullptr;       // sorted interface-node list (static per material)
   int* elist = nullptr;       // sorted active-element (non-void voxel) list
+  int* alist = nullptr;       // sorted active-node list (compact I/O; built on demand per material)
+  long long acount = 0;
+  bool alist_valid = false;
   int* l2list = nullptr;      // non-uniform level-2 elements (Galerkin build)
   uint8_t* eflag = nullptr;
   int ecount = 0;
   int* icount_d = nullptr;
-  int icount = 0;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int tntx = 0, tnty = 0;
@@ -510,12 +511,7 @@ int build_operators(gmt_problem p) {
       CK(cudaEventRecord(p->ev_u_ready, st));
     }
     thrust::counting_iterator<int> it(0);
-    CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->ilist, p->icount_d, (int)total, st));
     int cnt = 0;
-    CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (cnt != p->icount) drop_graph(p);   // grid size of the captured interface launch changes
-    p->icount = cnt;
     // active elements (s != 0) for the C^H reduction
     CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->eflag, p->elist, p->icount_d, (int)total, st));
     CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -630,6 +626,7 @@ int reset_solution(gmt_problem p, bool defer0 = false) {
 }
 
 int rebuild(gmt_problem p) {
+  p->alist_valid = false;
   // reset first: a following gmt_set_initial_guess upload only has to wait
   // for the reset, not for the operator build
   TRY(reset_solution(p, true));
@@ -817,7 +814,7 @@ void free_all(gmt_problem p) {
   cudaFree(p->M1g); cudaFree(p->M2g);
   if (p->tflag) cudaFree(p->tflag - (size_t)p->tntx * p->tnty * TF_GLO);
   cudaFree(p->iflag);
-  if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->ilist); cudaFree(p->elist); cudaFree(p->l2list); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
+  if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->elist); cudaFree(p->alist); cudaFree(p->l2list); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->ev_u_ready) cudaEventDestroy(p->ev_u_ready);
@@ -834,6 +831,23 @@ int check_level(gmt_problem p, int level, bool allow_coarsest = true) {
   if (p->grp) return fail(GMT_ERR_STATE, "row-level entry points act on single-device problems only");
   if (level < 0 || level >= p->L || (!allow_coarsest && level >= p->L - 1))
     return fail(GMT_ERR_ARG, "level %d out of range (L=%d)", level, p->L);
+  return GMT_OK;
+}
+
+// Sorted active-node list of the current material (on demand).
+int ensure_alist(gmt_problem p) {
+  if (p->alist_valid) return GMT_OK;
+  const size_t total = p->lv[0].nodes;
+  if (!p->alist) TRY(dalloc(p, (void**)&p->alist, total * sizeof(int)));
+  k_nonzero_flags<<<1184, 256, 0, p->stream>>>(p->code, total, p->iflag);
+  LAUNCHED(p);
+  thrust::counting_iterator<int> it(0);
+  CK(cub::DeviceSelect::Flagged(p->cub_tmp, p->cub_bytes, it, p->iflag, p->alist, p->icount_d, (int)total, p->stream));
+  int cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, p->icount_d, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  p->acount = cnt;
+  p->alist_valid = true;
   return GMT_OK;
 }
 
@@ -1061,7 +1075,6 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   if ((rc = dalloc(p, (void**)&p->iflag, p->lv[0].nodes))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->code, (p->lv[0].nodes + 2 * pl0) * sizeof(float)))) return bail(rc);
   p->code += pl0;   // node codes of planes -1 .. nz
-  if ((rc = dalloc(p, (void**)&p->ilist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->elist, p->lv[0].nodes * sizeof(int)))) return bail(rc);
   if (L >= 3 && (rc = dalloc(p, (void**)&p->l2list, p->lv[2].nodes * sizeof(int)))) return bail(rc);
   if ((rc = dalloc(p, (void**)&p->eflag, p->lv[0].nodes))) return bail(rc);
@@ -1069,7 +1082,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
   {
     thrust::counting_iterator<int> it(0);
     size_t bytes = 0;
-    if (cub::DeviceSelect::Flagged(nullptr, bytes, it, p->iflag, p->ilist, p->icount_d, (int)p->lv[0].nodes) !=
+    if (cub::DeviceSelect::Flagged(nullptr, bytes, it, p->iflag, p->elist, p->icount_d, (int)p->lv[0].nodes) !=
         cudaSuccess)
       return bail(fail(GMT_ERR_CUDA, "cub temp query failed"));
     p->cub_bytes = bytes;
@@ -1377,6 +1390,81 @@ int gmt_get_solution(gmt_problem p, float* u, int location, int zero_mean_flag) 
   if (zero_mean_flag) TRY(p->dpn == 3 ? zero_mean<3>(p, dst) : zero_mean<1>(p, dst));
   if (location == GMT_HOST) {
     CK(cudaMemcpyAsync(u, dst, b.nodes * p->V * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  }
+  return GMT_OK;
+}
+
+long long gmt_active_count(gmt_problem p) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  TRY(no_group(p));
+  TRY(set_device(p));
+  TRY(ensure_alist(p));
+  return p->acount;
+}
+
+int gmt_active_nodes(gmt_problem p, int32_t* nodes, int location) {
+  if (!p || !nodes) return fail(GMT_ERR_ARG, "null argument");
+  TRY(no_group(p));
+  TRY(set_device(p));
+  TRY(ensure_alist(p));
+  CK(cudaMemcpyAsync(nodes, p->alist, (size_t)p->acount * sizeof(int),
+                     location == GMT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, p->stream));
+  if (location == GMT_HOST) CK(cudaStreamSynchronize(p->stream));
+  return GMT_OK;
+}
+
+int gmt_set_initial_guess_compact(gmt_problem p, const float* u, int location) {
+  if (!p || !u) return fail(GMT_ERR_ARG, "null argument");
+  TRY(no_group(p));
+  p->u0_stale = false;   // every active value is overwritten (inactive ones are never read as data)
+  TRY(set_device(p, true));
+  p->refine = false;
+  TRY(ensure_alist(p));
+  LevelBuf& b = p->lv[0];
+  // on the copy stream after everything that touched u (see gmt_set_initial_guess);
+  // host data is staged in the residual buffer (scratch between cycles)
+  if (!p->u_ready_pending) CK(cudaEventRecord(p->ev_u_ready, p->stream));
+  p->u_ready_pending = false;
+  CK(cudaStreamWaitEvent(p->copy_stream, p->ev_u_ready, 0));
+  const size_t bytes = (size_t)p->acount * p->V * sizeof(float);
+  const float* src = u;
+  if (location == GMT_HOST) {
+    float* stage = vbase(b, b.r);
+    CK(cudaMemcpyAsync(stage, u, bytes, cudaMemcpyHostToDevice, p->copy_stream));
+    src = stage;
+  }
+  if (p->acount > 0) {
+    k_scatter_compact<<<1184, 256, 0, p->copy_stream>>>(p->alist, p->acount, src, b.u, b.cs, p->V);
+    LAUNCHED(p);
+  }
+  CK(cudaEventRecord(p->ev_copy, p->copy_stream));
+  CK(cudaStreamWaitEvent(p->stream, p->ev_copy, 0));
+  return GMT_OK;
+}
+
+int gmt_get_solution_compact(gmt_problem p, float* u, int location, int zero_mean_flag) {
+  if (!p || !u) return fail(GMT_ERR_ARG, "null argument");
+  TRY(no_group(p));
+  TRY(set_device(p));
+  TRY(ensure_alist(p));
+  LevelBuf& b = p->lv[0];
+  const long long A = p->acount;
+  float* dst = (location == GMT_DEVICE) ? u : vbase(b, b.r);
+  if (A > 0) {
+    k_gather_compact<<<1184, 256, 0, p->stream>>>(p->alist, A, p->refine ? p->uhi : b.u, dst, b.cs, p->V);
+    LAUNCHED(p);
+    if (zero_mean_flag) {
+      const int nblk = 296;
+      k_compact_sum<<<nblk, 256, 0, p->stream>>>(dst, A, p->V, p->part);
+      LAUNCHED(p);
+      TRY(reduce_launch(p, nblk, p->V + 1));
+      k_compact_sub_mean<<<1184, 256, 0, p->stream>>>(dst, A, p->V, p->red);
+      LAUNCHED(p);
+    }
+  }
+  if (location == GMT_HOST) {
+    CK(cudaMemcpyAsync(u, dst, (size_t)A * p->V * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
     CK(cudaStreamSynchronize(p->stream));
   }
   return GMT_OK;

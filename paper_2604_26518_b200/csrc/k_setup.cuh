@@ -357,3 +357,71 @@ k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S
 }
 
 }  // namespace gmt
+
+namespace gmt {
+
+// ---- compact active-node I/O (Sec. 4.1.1 sparse voxels)
+
+__global__ void k_nonzero_flags(const float* __restrict__ c, size_t n, uint8_t* __restrict__ flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    flag[i] = c[i] != 0.f ? 1 : 0;
+}
+
+// dst[k * cs + list[j]] = src[k * A + j]  (V components)
+__global__ void k_scatter_compact(const int* __restrict__ list, long long A, const float* __restrict__ src,
+                                  float* __restrict__ dst, ptrdiff_t cs, int V) {
+  const long long total = A * V;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / A, j = t - k * A;
+    dst[k * cs + __ldg(list + j)] = __ldcs(src + t);
+  }
+}
+
+// dst[k * A + j] = src[k * cs + list[j]]
+__global__ void k_gather_compact(const int* __restrict__ list, long long A, const float* __restrict__ src,
+                                 float* __restrict__ dst, ptrdiff_t cs, int V) {
+  const long long total = A * V;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / A, j = t - k * A;
+    dst[t] = __ldg(src + k * cs + __ldg(list + j));
+  }
+}
+
+// Per-component sums of a compact vector (block partials, V + 1 per block:
+// the V sums, then the count A once), deterministic order.
+__global__ void __launch_bounds__(256) k_compact_sum(const float* __restrict__ v, long long A, int V,
+                                                     double* __restrict__ part) {
+  __shared__ double sh[8];
+  for (int k = 0; k <= V; ++k) {
+    double a = 0.0;
+    if (k < V)
+      for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < A; j += (long long)gridDim.x * blockDim.x)
+        a += v[(long long)k * A + j];
+    else if (blockIdx.x == 0 && threadIdx.x == 0)
+      a = (double)A;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+      part[(long long)blockIdx.x * (V + 1) + k] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_compact_sub_mean(float* __restrict__ v, long long A, int V, const double* __restrict__ sums) {
+  const long long total = A * V;
+  const double cnt = sums[V];
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / A;
+    v[t] = (float)((double)v[t] - sums[k] / cnt);
+  }
+}
+
+}  // namespace gmt

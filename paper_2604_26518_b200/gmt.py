@@ -83,6 +83,10 @@ SIGNATURES = {
                                   C.c_void_p, C.POINTER(C.c_void_p)]),
     "gmt_num_slabs": (C.c_int, [_P]),
     "gmt_set_refinement": (C.c_int, [_P, C.c_int]),
+    "gmt_active_count": (C.c_longlong, [_P]),
+    "gmt_active_nodes": (C.c_int, [_P, C.c_void_p, C.c_int]),
+    "gmt_set_initial_guess_compact": (C.c_int, [_P, _FP, C.c_int]),
+    "gmt_get_solution_compact": (C.c_int, [_P, _FP, C.c_int, C.c_int]),
     "gmt_refinement_active": (C.c_int, [_P]),
 }
 
@@ -311,6 +315,44 @@ class Problem:
         ptr, loc = _buf(out, np.float32)
         _check_size(out, self._vsize(0))
         _check(self.lib.gmt_get_solution(self._h, ptr, loc, int(zero_mean)), "gmt_get_solution")
+        return out
+
+    # -- compact active-node I/O (Sec. 4.1.1) ---------------------------------
+    def gmt_active_count(self) -> int:
+        n = self.lib.gmt_active_count(self._h)
+        if n < 0:
+            _check(int(n), "gmt_active_count")
+        return int(n)
+
+    def compact_shape(self):
+        return (self.nrhs, self.dpn, self.gmt_active_count())
+
+    def gmt_active_nodes(self, out=None):
+        if out is None:
+            out = np.empty(self.gmt_active_count(), dtype=np.int32)
+        if isinstance(out, np.ndarray):
+            if out.dtype != np.int32 or not out.flags.c_contiguous:
+                raise TypeError("active-node list must be a contiguous int32 array")
+            ptr, loc = out.ctypes.data, GMT_HOST
+        else:
+            if not out.is_cuda or str(out.dtype) != "torch.int32" or not out.is_contiguous():
+                raise TypeError("active-node list must be a contiguous int32 CUDA tensor")
+            ptr, loc = out.data_ptr(), GMT_DEVICE
+        _check_size(out, self.gmt_active_count())
+        _check(self.lib.gmt_active_nodes(self._h, ptr, loc), "gmt_active_nodes")
+        return out
+
+    def gmt_set_initial_guess_compact(self, u):
+        ptr, loc = _buf(u, np.float32)
+        _check_size(u, int(np.prod(self.compact_shape())))
+        _check(self.lib.gmt_set_initial_guess_compact(self._h, ptr, loc), "gmt_set_initial_guess_compact")
+
+    def gmt_get_solution_compact(self, out=None, zero_mean: bool = False):
+        if out is None:
+            out = np.empty(self.compact_shape(), dtype=np.float32)
+        ptr, loc = _buf(out, np.float32)
+        _check_size(out, int(np.prod(self.compact_shape())))
+        _check(self.lib.gmt_get_solution_compact(self._h, ptr, loc, int(zero_mean)), "gmt_get_solution_compact")
         return out
 
     def gmt_set_refinement(self, mode: int):

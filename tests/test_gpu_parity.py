@@ -381,3 +381,36 @@ def test_level0_vcycle_kernel_one_sweep(case):
     assert np.all(err <= 1e-5 * sc[a2] + 1e-30), f"max ratio {(err / (1e-5 * sc[a2])).max():.2f}"
     r_o = fem.relative_residual(H.K[0], uf, H.f)
     assert np.allclose(r_g, r_o, rtol=1e-4), (r_g, r_o)
+
+
+def test_compact_active_node_io(case):
+    """Compact I/O on the active set (Sec. 4.1.1): the library's sorted
+    active-node list equals the oracle's active set (nodes with a nonzero
+    diagonal); a compact guess round-trips and matches the dense path; the
+    compact gauge (Sec. 4.5) equals the oracle's projection."""
+    kind, s, ph, H, P = case
+    n = s.shape[0]
+    act_nodes = np.flatnonzero(H.active[0].reshape(-1, ph.dpn)[:, 0])     # node = x + n (y + n z)
+    got = P.gmt_active_nodes()
+    assert np.array_equal(got, act_nodes.astype(np.int32))
+    A = len(act_nodes)
+    rng = np.random.default_rng(5)
+    uc = rng.standard_normal((ph.nrhs, ph.dpn, A)).astype(np.float32)
+    P.gmt_set_initial_guess_compact(uc)
+    assert np.array_equal(P.gmt_get_solution_compact(), uc)
+    dense = P.gmt_get_solution()
+    flat = dense.reshape(ph.nrhs, ph.dpn, -1)
+    assert np.array_equal(flat[:, :, act_nodes], uc)
+    mask = np.ones(flat.shape[2], bool)
+    mask[act_nodes] = False
+    assert not np.any(flat[:, :, mask])
+    zc = P.gmt_get_solution_compact(zero_mean=True).astype(np.float64)
+    want = gmg.project_zero_mean(from_gpu(dense), ph.dpn, H.active[0].reshape(-1, ph.dpn)[:, 0])
+    want = to_gpu(want, n, ph.dpn).reshape(ph.nrhs, ph.dpn, -1)[:, :, act_nodes]
+    assert np.abs(zc - want).max() <= 1e-6 * max(1.0, np.abs(want).max())
+    # device buffers take the same path
+    ud = torch.from_numpy(uc).cuda()
+    P.gmt_set_initial_guess_compact(ud)
+    out = torch.empty_like(ud)
+    P.gmt_get_solution_compact(out)
+    assert torch.equal(out, ud)
