@@ -140,6 +140,8 @@ def parse():
     ap.add_argument("--vf", type=float, default=0.3)
     ap.add_argument("--levels", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l0-kernel", type=int, default=0, choices=[0, 1],
+                    help="level-0 sweep: 0 CUDA-core sum-factorised stencil (k_l0), 1 tcgen05 element contractions")
     ap.add_argument("--no-like", action="store_true", help="skip the like-for-like GPU line at the sample size")
     ap.add_argument("--breakdown", action="store_true", help="extra pass with per-class event timing")
     ap.add_argument("--no-solve", action="store_true", help="skip the (untimed) full solve to 1e-5")
@@ -394,6 +396,7 @@ def main():
         P = Problem(s_dev, physics=args.physics, levels=args.levels, device=local, dist=(rank, world, nid))
     else:
         P = Problem(s_dev, physics=args.physics, levels=args.levels, device=local)
+    P.gmt_set_level0_kernel(args.l0_kernel)
     P.gmt_profile_enable(1)   # bracket the dominant kernel (level-0 Jacobi sweep) live
     st = torch.cuda.ExternalStream(P.stream)
 
@@ -539,7 +542,8 @@ def main():
         "config": {**workload_config(args), "levels": levels,
                    "parallelism": f"slab{world} (z-slabs, NCCL halos)" if dist else "single GPU"},
         "vcycles_per_s": 1e3 / ms, "vcycle_ms": vc_ms, "active_nodes": n_act, "active_dof_x_cases": dofs,
-        "roofline": {"bound": "hbm", "kernel": "level-0 damped-Jacobi sweep (k_l0)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "level-0 damped-Jacobi sweep (" + ("k_l0_tc, tcgen05" if args.l0_kernel else "k_l0") + ")",
                      "achieved": achieved, "peak": hbm_agg, "unit": "GB/s", "frac": achieved / hbm_agg,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": hbm_src,
                      "bytes_per_launch": bytes_launch,

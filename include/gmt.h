@@ -147,6 +147,15 @@ GMT_API int gmt_residual_norms(gmt_problem p, double* rel, double* abs_r, double
  * gmt_set_initial_guess leave refinement.  Slab-partitioned problems refine
  * the same way (the hi / lo ghost planes are exchanged for the defect). */
 GMT_API int gmt_set_refinement(gmt_problem p, int mode);
+/* Level-0 sweep implementation (rows A1-A3): 0 = k_l0, CUDA-core
+ * sum-factorised stencil (default); 1 = k_l0_tc, the tensor-core variant
+ * named by the north star: Sec. 4.6 Eq. 14 as batched element contractions
+ * U_e K_e^T on tcgen05 (kind::tf32, 3xTF32 split for fp32 accuracy, TMEM
+ * accumulators).  Same results to rounding; kept for the A/B measurement
+ * (DESIGN.md "Tensor cores").  Synchronises the stream; drops the captured
+ * V-cycle graph.  Errors: GMT_ERR_ARG. */
+GMT_API int gmt_set_level0_kernel(gmt_problem p, int kind);
+
 /* 1 while the problem is in refinement, 0 otherwise. */
 GMT_API int gmt_refinement_active(gmt_problem p);
 

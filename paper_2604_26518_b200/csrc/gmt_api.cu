@@ -23,6 +23,7 @@
 #include "gmt_fem.h"
 #include "k_coarse_tiled.cuh"
 #include "k_l0.cuh"
+#include "k_l0_tc.cuh"
 #include "k_level.cuh"
 #include "k_reduce.cuh"
 #include "k_setup.cuh"
@@ -151,6 +152,8 @@ struct gmt_problem_s {
   size_t cub_bytes = 0;
   int tntx = 0, tnty = 0;
   L0Consts l0c{};             // level-0 sweep constants (k_l0)
+  TcB* tcb = nullptr;         // K_e as the tf32 hi/lo B operand of the tensor-core variant (k_l0_tc)
+  int l0_kernel = 0;          // 0: k_l0 (CUDA cores, default), 1: k_l0_tc (tcgen05)
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
@@ -308,6 +311,12 @@ dim3 l0_grid(gmt_problem p) {
   return dim3((b.n + L0_X - 1) / L0_X, (b.n + L0_Y - 1) / L0_Y, ((b.nz + L0_ZC - 1) / L0_ZC) * NG);
 }
 template <int DPN>
+dim3 tc_grid(gmt_problem p) {
+  const LevelBuf& b = p->lv[0];
+  constexpr int NG = Tr<DPN>::NR / L0V<DPN>::NRG;
+  return dim3((b.n + TC_NX - 1) / TC_NX, (b.n + TC_NY - 1) / TC_NY, ((b.nz + TC_ZC - 1) / TC_ZC) * NG);
+}
+template <int DPN>
 constexpr size_t l0_smem() {
   return (size_t)L0_NB * (L0V<DPN>::NRG * DPN * L0_PLS + L0_CPL) * sizeof(float);
 }
@@ -321,7 +330,25 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   const float om = (float)p->cfg.omega;
   Prof prof(p, l == 0 ? (mode == M_JACOBI ? 0 : (mode == M_RESID ? 1 : 31)) : 4);
   const ptrdiff_t cs = b.cs;
-  if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
+  if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID) && p->l0_kernel == 1) {
+    // tensor-core element-contraction variant (k_l0_tc.cuh)
+    const ZMap z = p->zm(0);
+    const dim3 grid = tc_grid<DPN>(p);
+    const size_t shm = tc_smem_bytes<DPN>();
+    if (f) {
+      if (mode == M_JACOBI)
+        k_l0_tc<DPN, M_JACOBI, true><<<grid, 128, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->l0c, p->tcb, part, cs, f);
+      else
+        k_l0_tc<DPN, M_RESID, true><<<grid, 128, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->l0c, p->tcb, part, cs, f);
+    } else {
+      if (mode == M_JACOBI)
+        k_l0_tc<DPN, M_JACOBI, false><<<grid, 128, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->l0c, p->tcb, part, cs,
+                                                               nullptr);
+      else
+        k_l0_tc<DPN, M_RESID, false><<<grid, 128, shm, st>>>(p->s, z, u, z, out, b.n, b.nz, p->l0c, p->tcb, part, cs,
+                                                              nullptr);
+    }
+  } else if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
     // the V-cycle's level-0 sweep: uniform + interface nodes in one launch
     const ZMap z = p->zm(0);
     const dim3 grid = l0_grid<DPN>(p), block(L0_X, L0_TY);
@@ -679,7 +706,7 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
 // Number of fp64 partial rows the level-0 residual launch writes (one per CTA).
 template <int DPN>
 int l0_partials(gmt_problem p, bool /*fexp*/) {
-  const dim3 g = l0_grid<DPN>(p);
+  const dim3 g = p->l0_kernel == 1 ? tc_grid<DPN>(p) : l0_grid<DPN>(p);
   return (int)(g.x * g.y * g.z);
 }
 
@@ -811,7 +838,7 @@ void free_all(gmt_problem p) {
   for (float* v : {p->uhi, p->ulo, p->f0})
     if (v && !p->lv.empty()) cudaFree(vbase(p->lv[0], v));
   if (p->s) cudaFree(p->s - (size_t)p->N * p->N * MAT_GLO);
-  cudaFree(p->M1g); cudaFree(p->M2g);
+  cudaFree(p->M1g); cudaFree(p->M2g); cudaFree(p->tcb);
   if (p->tflag) cudaFree(p->tflag - (size_t)p->tntx * p->tnty * TF_GLO);
   cudaFree(p->iflag);
   if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->elist); cudaFree(p->alist); cudaFree(p->l2list); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
@@ -1052,9 +1079,11 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     // sums x (V + 1); then the reduction stage area
     const int nr = p->nr, nq = nr * (nr + 1) / 2;
     const dim3 g0 = p->dpn == 3 ? l0_grid<3>(p) : l0_grid<1>(p);
+    const dim3 gt = p->dpn == 3 ? tc_grid<3>(p) : tc_grid<1>(p);
     const dim3 gz = zsum_grid(p->lv[0]);
     const size_t chg = (size_t)(p->dpn == 3 ? ch_grid<3>() : ch_grid<1>());
     size_t rows = std::max((size_t)g0.x * g0.y * g0.z * 2 * nr, chg * nq);
+    rows = std::max(rows, (size_t)gt.x * gt.y * gt.z * 2 * nr);
     rows = std::max(rows, (size_t)gz.x * gz.y * gz.z * (V + 1));
     p->part_cap = rows + (size_t)RED_BLOCKS * 64;
   }
@@ -1103,7 +1132,15 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_l0<1, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
         cudaFuncSetAttribute(k_l0<1, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
         cudaFuncSetAttribute(k_l0<1, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
-        cudaFuncSetAttribute(k_l0<1, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1))
+        cudaFuncSetAttribute(k_l0<1, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
+        cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
+        cudaFuncSetAttribute(k_l0_tc<3, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
+        cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
+        cudaFuncSetAttribute(k_l0_tc<3, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
+        cudaFuncSetAttribute(k_l0_tc<1, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<1>()) ||
+        cudaFuncSetAttribute(k_l0_tc<1, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<1>()) ||
+        cudaFuncSetAttribute(k_l0_tc<1, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<1>()) ||
+        cudaFuncSetAttribute(k_l0_tc<1, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<1>()))
       return bail(fail(GMT_ERR_CUDA, "cudaFuncSetAttribute failed"));
   }
   if ((rc = dalloc(p, (void**)&p->M1g, 8 * nd * nd * sizeof(float)))) return bail(rc);
@@ -1114,6 +1151,28 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
       for (int i = 0; i < nd * nd; ++i) m2[g * nd * nd + i] = (float)p->ed.M2[g][i];
     if (cudaMemcpy(p->M2g, m2.data(), m2.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(GMT_ERR_CUDA, "M2 upload failed"));
+  }
+  {
+    // K_e (current material scalars) as the tensor-core B operand, tf32 hi + lo
+    auto tf32 = [](float x) {
+      uint32_t b;
+      std::memcpy(&b, &x, 4);
+      b = (b + 0x1000u) & 0xFFFFE000u;   // round to nearest (ties away), 10-bit mantissa
+      float r;
+      std::memcpy(&r, &b, 4);
+      return r;
+    };
+    TcB hb{};
+    for (int r = 0; r < nd; ++r)
+      for (int c = 0; c < nd; ++c) {
+        const float v = (float)p->ed.K[r * nd + c];
+        const float h = tf32(v);
+        hb.hi[r * TC_K + c] = h;
+        hb.lo[r * TC_K + c] = tf32(v - h);
+      }
+    if ((rc = dalloc(p, (void**)&p->tcb, sizeof(TcB)))) return bail(rc);
+    if (cudaMemcpy(p->tcb, &hb, sizeof(TcB), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(GMT_ERR_CUDA, "tensor-core operand upload failed"));
   }
   if (cudaMallocHost(&p->hred, 64 * sizeof(double)) != cudaSuccess)
     return bail(fail(GMT_ERR_NOMEM, "cudaMallocHost failed"));
@@ -1630,6 +1689,20 @@ int gmt_set_refinement(gmt_problem p, int mode) {
       q->refine = false;
     }
   }
+  return GMT_OK;
+}
+
+int gmt_set_level0_kernel(gmt_problem p, int kind) {
+  if (!p) return fail(GMT_ERR_ARG, "null problem");
+  if (kind != 0 && kind != 1) return fail(GMT_ERR_ARG, "level-0 kernel must be 0 (CUDA cores) or 1 (tensor cores)");
+  TRY(set_device(p));
+  std::vector<gmt_problem> parts = p->grp ? p->grp->slabs : std::vector<gmt_problem>{p};
+  CK(cudaStreamSynchronize(p->stream));
+  for (auto q : parts)
+    if (q->l0_kernel != kind) {
+      q->l0_kernel = kind;
+      drop_graph(q);
+    }
   return GMT_OK;
 }
 

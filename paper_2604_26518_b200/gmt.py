@@ -84,6 +84,7 @@ SIGNATURES = {
     "gmt_num_slabs": (C.c_int, [_P]),
     "gmt_set_refinement": (C.c_int, [_P, C.c_int]),
     "gmt_active_count": (C.c_longlong, [_P]),
+    "gmt_set_level0_kernel": (C.c_int, [_P, C.c_int]),
     "gmt_active_nodes": (C.c_int, [_P, C.c_void_p, C.c_int]),
     "gmt_set_initial_guess_compact": (C.c_int, [_P, _FP, C.c_int]),
     "gmt_get_solution_compact": (C.c_int, [_P, _FP, C.c_int, C.c_int]),
@@ -358,6 +359,10 @@ class Problem:
     def gmt_set_refinement(self, mode: int):
         """0 auto (default), 1 off, 2 on: mixed-precision iterative refinement."""
         _check(self.lib.gmt_set_refinement(self._h, int(mode)), "gmt_set_refinement")
+
+    def gmt_set_level0_kernel(self, kind: int):
+        """0: CUDA-core sum-factorised stencil (default), 1: tcgen05 element contractions."""
+        _check(self.lib.gmt_set_level0_kernel(self._h, int(kind)), "gmt_set_level0_kernel")
 
     def gmt_refinement_active(self) -> bool:
         return bool(self.lib.gmt_refinement_active(self._h))

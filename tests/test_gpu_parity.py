@@ -356,12 +356,14 @@ def test_material_reset_and_initial_guess(kind):
     assert np.array_equal(P.gmt_get_solution(), a)
 
 
-def test_level0_vcycle_kernel_one_sweep(case):
+@pytest.mark.parametrize("l0kernel", [0, 1], ids=["k_l0", "k_l0_tc"])
+def test_level0_vcycle_kernel_one_sweep(case, l0kernel):
     """The V-cycle's level-0 kernel itself (k_l0: uniform nodes sum-factorised,
-    interface nodes from the staged planes): with one level and one coarsest
-    sweep, gmt_vcycle is exactly one damped-Jacobi sweep (Sec. 4.6 Eq. 16),
-    compared element by element with the oracle at every active node; then
-    its residual mode through gmt_residual_norms (Sec. 5.2) on the same u."""
+    interface nodes from the staged planes; k_l0_tc: element contractions on
+    tcgen05 tensor cores, 3xTF32): with one level and one coarsest sweep,
+    gmt_vcycle is exactly one damped-Jacobi sweep (Sec. 4.6 Eq. 16), compared
+    element by element with the oracle at every active node; then its
+    residual mode through gmt_residual_norms (Sec. 5.2) on the same u."""
     kind, s, ph, H, _ = case
     n = s.shape[0]
     rng = np.random.default_rng(21)
@@ -369,6 +371,7 @@ def test_level0_vcycle_kernel_one_sweep(case):
     u = rng.standard_normal(H.f.shape) * act[:, None] + 0.3 * n * np.sin(np.arange(H.f.shape[0]))[:, None] * act[:, None]
     want = gmg.jacobi(H.K[0], H.Dinv[0], u, H.f, OMEGA[kind], 1)
     with _problem(s, kind, 1, coarse_sweeps=1) as P1:
+        P1.gmt_set_level0_kernel(l0kernel)
         P1.gmt_set_initial_guess(np.ascontiguousarray(to_gpu(u, n, ph.dpn), dtype=np.float32))
         r_g, ar_g, af_g = P1.gmt_residual_norms()
         P1.gmt_vcycle(1)
@@ -414,3 +417,18 @@ def test_compact_active_node_io(case):
     out = torch.empty_like(ud)
     P.gmt_get_solution_compact(out)
     assert torch.equal(out, ud)
+
+
+def test_tensor_core_variant_vcycles(case):
+    """The tcgen05 variant inside full V-cycles (and iterative-refinement's
+    explicit right-hand side): the same solution as the CUDA-core kernel to
+    fp32 rounding, cycle after cycle."""
+    kind, s, ph, H, P = case
+    L = H.L
+    with _problem(s, kind, L) as A, _problem(s, kind, L) as B:
+        B.gmt_set_level0_kernel(1)
+        for P_ in (A, B):
+            P_.gmt_set_refinement(2)
+            P_.gmt_vcycle(3)
+        ua, ub = A.gmt_get_solution(), B.gmt_get_solution()
+    assert np.abs(ub - ua).max() <= 1e-4 * np.abs(ua).max()
