@@ -195,6 +195,27 @@ GMT_API int gmt_active_nodes(gmt_problem p, int32_t* nodes, int location);
 GMT_API int gmt_set_initial_guess_compact(gmt_problem p, const float* u_active, int location);
 GMT_API int gmt_get_solution_compact(gmt_problem p, float* u_active, int location, int zero_mean);
 
+/* Batches of independent problems on one GPU (BASELINE configs[2]:
+ * high-throughput screening of many unit cells, Sec. 7.1 / App. C).  A batch
+ * borrows `count` single-device problems created on the same device (they
+ * must outlive it and are still usable on their own).  gmt_batch_vcycle runs
+ * one V-cycle of every problem per cycle as ONE CUDA-graph launch: the
+ * problems' V-cycles are captured side by side (one graph branch per
+ * problem stream) and replayed concurrently; the graph is re-captured when a
+ * problem's operators change shape.  It is ordered after all work already
+ * enqueued on the problems' streams and before work enqueued later.
+ * Problems in iterative refinement or with a pending injection are cycled
+ * one by one instead.  gmt_batch_homogenize / gmt_batch_residual_norms
+ * write count * NRHS^2 (C^H, row-major per problem) / count * NRHS (relative
+ * residuals) host doubles with one synchronisation.  Errors: GMT_ERR_ARG
+ * (empty batch, slab problems, mixed devices), GMT_ERR_CUDA. */
+typedef struct gmt_batch_s* gmt_batch;
+GMT_API int gmt_batch_create(gmt_problem* problems, int count, gmt_batch* out);
+GMT_API int gmt_batch_vcycle(gmt_batch b, int ncycles);
+GMT_API int gmt_batch_homogenize(gmt_batch b, double* CH);
+GMT_API int gmt_batch_residual_norms(gmt_batch b, double* rel);
+GMT_API void gmt_batch_destroy(gmt_batch b);
+
 /* Problem properties. */
 GMT_API int gmt_num_levels(gmt_problem p);
 GMT_API int gmt_level_res(gmt_problem p, int level);      /* n_l */

@@ -157,6 +157,7 @@ struct gmt_problem_s {
   size_t bytes = 0;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
+  long long graph_gen = 0;    // bumped whenever captured launches become stale (batch graphs compare it)
   // mixed-precision iterative refinement (level 0): the solution is held as
   // an unevaluated fp32 sum hi + lo; V-cycles run on the fp32 correction with
   // the defect f - K (hi + lo) as explicit right-hand side
@@ -679,8 +680,9 @@ int reduce(gmt_problem p, int nblk, int nv) {
   return GMT_OK;
 }
 
+// C^H kernel + reduction + asynchronous copy of the NQ sums to p->hred.
 template <int DPN>
-int effective_tensor(gmt_problem p, const float* u, double* CH) {
+int effective_tensor_launch(gmt_problem p, const float* u) {
   constexpr int NR = Tr<DPN>::NR, NQ = NR * (NR + 1) / 2;
   const LevelBuf& b = p->lv[0];
   const int nblk = std::max(1, std::min((GMT_CH_ITEMS * p->ecount + CH_THREADS - 1) / CH_THREADS, ch_grid<DPN>()));
@@ -691,7 +693,15 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
                                                          p->ecount);
     LAUNCHED(p);
   }
-  TRY(reduce(p, nblk, NQ));
+  TRY(reduce_launch(p, nblk, NQ));
+  CK(cudaMemcpyAsync(p->hred, p->red, NQ * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  return GMT_OK;
+}
+
+// C^H from the sums in p->hred (after the stream synchronised).
+template <int DPN>
+void effective_tensor_finish(gmt_problem p, double* CH) {
+  constexpr int NR = Tr<DPN>::NR;
   const double vol = (double)p->N * p->N * p->N;
   int qi = 0;
   for (int m = 0; m < NR; ++m)
@@ -700,6 +710,13 @@ int effective_tensor(gmt_problem p, const float* u, double* CH) {
       CH[m * NR + n] = v;
       CH[n * NR + m] = v;
     }
+}
+
+template <int DPN>
+int effective_tensor(gmt_problem p, const float* u, double* CH) {
+  TRY(effective_tensor_launch<DPN>(p, u));
+  CK(cudaStreamSynchronize(p->stream));
+  effective_tensor_finish<DPN>(p, CH);
   return GMT_OK;
 }
 
@@ -711,12 +728,21 @@ int l0_partials(gmt_problem p, bool /*fexp*/) {
 }
 
 template <int DPN>
+int residual_norms_launch(gmt_problem p) {
+  constexpr int NR = Tr<DPN>::NR;
+  LevelBuf& b = p->lv[0];
+  TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
+  TRY(reduce_launch(p, l0_partials<DPN>(p, false), 2 * NR));
+  CK(cudaMemcpyAsync(p->hred, p->red, 2 * NR * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  return GMT_OK;
+}
+
+template <int DPN>
 int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
   constexpr int NR = Tr<DPN>::NR;
   LevelBuf& b = p->lv[0];
-  const Geo g = geo(b.n, b.nz);
-  // tiled path (skip_void): r keeps zeros at inactive nodes, partials per CTA
-  // of the tiled kernel followed by those of the interface kernel
+  // level-0 sweep kernel in residual mode: r keeps zeros at inactive nodes,
+  // per-CTA partials of r^2 and f^2
   TRY(launch_op<DPN>(p, 0, M_RESID, b.u, nullptr, b.r, p->part, 1));
   TRY(reduce(p, l0_partials<DPN>(p, false), 2 * NR));
   for (int m = 0; m < NR; ++m) {
@@ -811,6 +837,7 @@ int zero_mean(gmt_problem p, float* dst) {
 }
 
 void drop_graph(gmt_problem p) {
+  ++p->graph_gen;
   if (p->grp) drop_group_graph(p->grp);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   p->gexec = nullptr;
@@ -1527,6 +1554,181 @@ int gmt_get_solution_compact(gmt_problem p, float* u, int location, int zero_mea
     CK(cudaStreamSynchronize(p->stream));
   }
   return GMT_OK;
+}
+
+}  // extern "C"
+
+struct gmt_batch_s {
+  std::vector<gmt_problem> ps;
+  cudaStream_t master = nullptr;
+  cudaEvent_t fork = nullptr, done = nullptr;
+  std::vector<cudaEvent_t> ready, joins;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<long long> gens;            // graph generations of the problems at capture
+  std::vector<long long> kernels;         // kernels per problem in the captured graph
+};
+
+namespace {
+
+void batch_drop(gmt_batch b) {
+  if (b->gexec) cudaGraphExecDestroy(b->gexec);
+  b->gexec = nullptr;
+  b->gens.clear();
+}
+
+// One V-cycle of every problem as a single graph launch on the batch's stream.
+int batch_cycle_graph(gmt_batch b) {
+  const size_t n = b->ps.size();
+  std::vector<long long> gens(n);
+  for (size_t i = 0; i < n; ++i) gens[i] = b->ps[i]->graph_gen;
+  if (!b->gexec || gens != b->gens) {
+    batch_drop(b);
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(b->master, cudaStreamCaptureModeRelaxed));
+    CK(cudaEventRecord(b->fork, b->master));
+    int rc = GMT_OK;
+    b->kernels.assign(n, 0);
+    for (size_t i = 0; i < n && rc == GMT_OK; ++i) {
+      gmt_problem p = b->ps[i];
+      if (cudaStreamWaitEvent(p->stream, b->fork, 0) != cudaSuccess) { rc = fail(GMT_ERR_CUDA, "fork"); break; }
+      p->capturing = true;
+      p->capture_count = 0;
+      const unsigned mask = p->prof_mask;   // no profiling brackets inside a batch graph
+      p->prof_mask = 0;
+      rc = vcycle_dispatch(p);
+      p->prof_mask = mask;
+      p->capturing = false;
+      b->kernels[i] = p->capture_count;
+      if (rc == GMT_OK && (cudaEventRecord(b->joins[i], p->stream) != cudaSuccess ||
+                           cudaStreamWaitEvent(b->master, b->joins[i], 0) != cudaSuccess))
+        rc = fail(GMT_ERR_CUDA, "join");
+    }
+    cudaError_t ec = cudaStreamEndCapture(b->master, &g);
+    if (rc != GMT_OK) { if (g) cudaGraphDestroy(g); return rc; }
+    if (ec != cudaSuccess) return fail(GMT_ERR_CUDA, "batch graph capture failed: %s", cudaGetErrorString(ec));
+    ec = cudaGraphInstantiate(&b->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ec != cudaSuccess) return fail(GMT_ERR_CUDA, "batch graph instantiate failed: %s", cudaGetErrorString(ec));
+    b->gens = gens;
+  }
+  // after everything already queued on the problems' streams ...
+  for (size_t i = 0; i < n; ++i) {
+    CK(cudaEventRecord(b->ready[i], b->ps[i]->stream));
+    CK(cudaStreamWaitEvent(b->master, b->ready[i], 0));
+  }
+  CK(cudaGraphLaunch(b->gexec, b->master));
+  // ... and before anything queued later
+  CK(cudaEventRecord(b->done, b->master));
+  for (size_t i = 0; i < n; ++i) {
+    CK(cudaStreamWaitEvent(b->ps[i]->stream, b->done, 0));
+    b->ps[i]->launches += b->kernels[i];
+  }
+  return GMT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gmt_batch_create(gmt_problem* problems, int count, gmt_batch* out) {
+  if (!problems || count <= 0 || !out) return fail(GMT_ERR_ARG, "empty batch");
+  *out = nullptr;
+  const int dev = problems[0] ? problems[0]->cfg.device : -1;
+  for (int i = 0; i < count; ++i) {
+    gmt_problem p = problems[i];
+    if (!p) return fail(GMT_ERR_ARG, "null problem in batch");
+    if (p->grp) return fail(GMT_ERR_ARG, "batches take single-device problems");
+    if (p->cfg.device != dev) return fail(GMT_ERR_ARG, "batch problems must share a device");
+  }
+  CK(cudaSetDevice(dev));
+  gmt_batch b = new gmt_batch_s();
+  b->ps.assign(problems, problems + count);
+  bool ok = cudaStreamCreateWithFlags(&b->master, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&b->fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&b->done, cudaEventDisableTiming) == cudaSuccess;
+  b->ready.assign(count, nullptr);
+  b->joins.assign(count, nullptr);
+  for (int i = 0; ok && i < count; ++i)
+    ok = cudaEventCreateWithFlags(&b->ready[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&b->joins[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    gmt_batch_destroy(b);
+    return fail(GMT_ERR_CUDA, "batch stream / event creation failed");
+  }
+  *out = b;
+  return GMT_OK;
+}
+
+int gmt_batch_vcycle(gmt_batch b, int ncycles) {
+  if (!b) return fail(GMT_ERR_ARG, "null batch");
+  if (ncycles < 0) return fail(GMT_ERR_ARG, "ncycles < 0");
+  bool plain = true;
+  for (auto p : b->ps) {
+    TRY(set_device(p));
+    bool inj = false;
+    for (auto& lb : p->lv) inj |= lb.inj_pending;
+    plain &= !p->refine && !inj && p->cfg.use_graphs;
+  }
+  for (int c = 0; c < ncycles; ++c) {
+    if (plain) {
+      TRY(batch_cycle_graph(b));
+    } else {
+      for (auto p : b->ps) TRY(gmt_vcycle(p, 1));
+    }
+  }
+  return GMT_OK;
+}
+
+int gmt_batch_homogenize(gmt_batch b, double* CH) {
+  if (!b || !CH) return fail(GMT_ERR_ARG, "null argument");
+  for (auto p : b->ps) {
+    TRY(set_device(p));
+    const float* u = p->refine ? p->uhi : p->lv[0].u;
+    TRY(p->dpn == 3 ? effective_tensor_launch<3>(p, u) : effective_tensor_launch<1>(p, u));
+  }
+  size_t off = 0;
+  for (auto p : b->ps) {
+    CK(cudaStreamSynchronize(p->stream));
+    if (p->dpn == 3) effective_tensor_finish<3>(p, CH + off);
+    else effective_tensor_finish<1>(p, CH + off);
+    off += (size_t)p->nr * p->nr;
+  }
+  return GMT_OK;
+}
+
+int gmt_batch_residual_norms(gmt_batch b, double* rel) {
+  if (!b || !rel) return fail(GMT_ERR_ARG, "null argument");
+  for (auto p : b->ps) {
+    TRY(set_device(p));
+    if (p->refine) continue;   // refinement: evaluated one by one below
+    TRY(p->dpn == 3 ? residual_norms_launch<3>(p) : residual_norms_launch<1>(p));
+  }
+  size_t off = 0;
+  for (auto p : b->ps) {
+    if (p->refine) {
+      TRY(gmt_residual_norms(p, rel + off, nullptr, nullptr));
+    } else {
+      CK(cudaStreamSynchronize(p->stream));
+      for (int m = 0; m < p->nr; ++m) {
+        const double nr_ = std::sqrt(p->hred[m]), nf = std::sqrt(p->hred[p->nr + m]);
+        rel[off + m] = nf > 0 ? nr_ / nf : nr_;
+      }
+    }
+    off += p->nr;
+  }
+  return GMT_OK;
+}
+
+void gmt_batch_destroy(gmt_batch b) {
+  if (!b) return;
+  if (b->master) cudaStreamSynchronize(b->master);
+  batch_drop(b);
+  for (auto e : b->ready) if (e) cudaEventDestroy(e);
+  for (auto e : b->joins) if (e) cudaEventDestroy(e);
+  if (b->fork) cudaEventDestroy(b->fork);
+  if (b->done) cudaEventDestroy(b->done);
+  if (b->master) cudaStreamDestroy(b->master);
+  delete b;
 }
 
 int gmt_num_levels(gmt_problem p) { return p ? p->L : GMT_ERR_ARG; }

@@ -85,6 +85,11 @@ SIGNATURES = {
     "gmt_set_refinement": (C.c_int, [_P, C.c_int]),
     "gmt_active_count": (C.c_longlong, [_P]),
     "gmt_set_level0_kernel": (C.c_int, [_P, C.c_int]),
+    "gmt_batch_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
+    "gmt_batch_vcycle": (C.c_int, [_P, C.c_int]),
+    "gmt_batch_homogenize": (C.c_int, [_P, _DP]),
+    "gmt_batch_residual_norms": (C.c_int, [_P, _DP]),
+    "gmt_batch_destroy": (None, [_P]),
     "gmt_active_nodes": (C.c_int, [_P, C.c_void_p, C.c_int]),
     "gmt_set_initial_guess_compact": (C.c_int, [_P, _FP, C.c_int]),
     "gmt_get_solution_compact": (C.c_int, [_P, _FP, C.c_int, C.c_int]),
@@ -426,3 +431,51 @@ class Problem:
         CH = (C.c_double * (self.nrhs * self.nrhs))()
         _check(self.lib.gmt_op_effective_tensor(self._h, _dptr(u, self._vsize(0)), CH), "gmt_op_effective_tensor")
         return np.array(CH).reshape(self.nrhs, self.nrhs)
+
+
+class Batch:
+    """A batch of independent problems on one GPU (gmt_batch_*): one CUDA-graph
+    launch per V-cycle of all of them, C^H / residual norms with one
+    synchronisation.  The problems must outlive the batch."""
+
+    def __init__(self, problems):
+        lib = load()
+        self.lib = lib
+        self.problems = list(problems)
+        arr = (C.c_void_p * len(self.problems))(*[P._h.value for P in self.problems])
+        h = C.c_void_p()
+        _check(lib.gmt_batch_create(arr, len(self.problems), C.byref(h)), "gmt_batch_create")
+        self._h = h
+
+    def gmt_batch_vcycle(self, ncycles: int = 1):
+        _check(self.lib.gmt_batch_vcycle(self._h, ncycles), "gmt_batch_vcycle")
+
+    def gmt_batch_homogenize(self):
+        nr = self.problems[0].nrhs
+        out = (C.c_double * (len(self.problems) * nr * nr))()
+        _check(self.lib.gmt_batch_homogenize(self._h, out), "gmt_batch_homogenize")
+        return np.array(out).reshape(len(self.problems), nr, nr)
+
+    def gmt_batch_residual_norms(self):
+        nr = self.problems[0].nrhs
+        out = (C.c_double * (len(self.problems) * nr))()
+        _check(self.lib.gmt_batch_residual_norms(self._h, out), "gmt_batch_residual_norms")
+        return np.array(out).reshape(len(self.problems), nr)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.gmt_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+

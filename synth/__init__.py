@@ -85,21 +85,30 @@ def tpms(n: int, kind: str = "gyroid", vf: float = 0.3, sheet: bool = False) -> 
     return _threshold_to_vf(phi, vf, below=True)
 
 
-def _periodic_segment_distance(p: np.ndarray, a: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """Distance from points p (..., 3) to segment a-b on the unit torus
-    (minimum over the 27 periodic images of the segment)."""
+def _periodic_segment_distance(p: np.ndarray, a: np.ndarray, b: np.ndarray, cutoff: float | None = None) -> np.ndarray:
+    """Distance from points p (..., 3) in [0,1]^3 to segment a-b on the unit
+    torus (minimum over the 27 periodic images of the segment).  With a
+    cutoff, images whose bounding box grown by the cutoff misses [0,1]^3 are
+    skipped: every point is farther than the cutoff from them, so the answer
+    to "distance <= cutoff" is unchanged (only distances above it may be
+    overestimated)."""
     best = None
     ab = b - a
     L2 = float(ab @ ab)
+    lo, hi = np.minimum(a, b), np.maximum(a, b)
     for ox in (-1, 0, 1):
         for oy in (-1, 0, 1):
             for oz in (-1, 0, 1):
                 o = np.array([ox, oy, oz], dtype=p.dtype)
+                if cutoff is not None and (np.any(hi + o + cutoff < 0.0) or np.any(lo + o - cutoff > 1.0)):
+                    continue
                 ap = p - (a + o)
                 t = np.clip((ap @ ab) / L2, 0.0, 1.0)
                 d = ap - t[..., None] * ab
                 dist = np.sqrt(np.einsum("...i,...i->...", d, d))
                 best = dist if best is None else np.minimum(best, dist)
+    if best is None:
+        best = np.full(p.shape[:-1], np.inf, dtype=p.dtype)
     return best
 
 
@@ -119,22 +128,59 @@ _TRUSS_EDGES = {
 def truss(n: int, kind: str = "bcc", radius: float = 0.08, cells: int = 1,
           extra_struts=None) -> np.ndarray:
     """Truss lattice (Appendix C (b)): cylindrical struts of the given radius
-    (unit-cell units) between lattice nodes, repeated ``cells`` times per axis."""
+    (unit-cell units) between lattice nodes, repeated ``cells`` times per axis.
+    A voxel is solid when its centre lies within ``radius`` of a strut on the
+    unit torus.  Each strut is cut into short pieces and every periodic image
+    of a piece is tested only on the voxels of its bounding box grown by the
+    radius (the union of the pieces' capsules is the strut's capsule)."""
     edges = list(_TRUSS_EDGES[kind]) if kind else []
     if extra_struts:
         edges += list(extra_struts)
-    out = np.zeros((n, n, n), dtype=np.float32)
-    t = _axes(n) * cells % 1.0
-    chunk = max(1, (1 << 21) // (n * n))
-    for z0 in range(0, n, chunk):
-        z1 = min(n, z0 + chunk)
-        P = np.stack(np.meshgrid(t[z0:z1], t, t, indexing="ij"), axis=-1)[..., ::-1]  # (z,y,x)->(x,y,z)
-        d = None
-        for a, b in edges:
-            da = _periodic_segment_distance(P, np.asarray(a, float), np.asarray(b, float))
-            d = da if d is None else np.minimum(d, da)
-        out[z0:z1] = (d <= radius).astype(np.float32)
-    return out
+    if cells > 1 and n % cells == 0:
+        one = truss(n // cells, kind, radius, 1, extra_struts)
+        return np.ascontiguousarray(np.tile(one, (cells, cells, cells)))
+    if cells > 1:   # cell size not a whole number of voxels: evaluate everywhere
+        out = np.zeros((n, n, n), dtype=np.float32)
+        t = _axes(n) * cells % 1.0
+        chunk = max(1, (1 << 21) // (n * n))
+        for z0 in range(0, n, chunk):
+            z1 = min(n, z0 + chunk)
+            P = np.stack(np.meshgrid(t[z0:z1], t, t, indexing="ij"), axis=-1)[..., ::-1]
+            d = None
+            for a, b in edges:
+                da = _periodic_segment_distance(P, np.asarray(a, float), np.asarray(b, float), cutoff=radius)
+                d = da if d is None else np.minimum(d, da)
+            out[z0:z1] = (d <= radius).astype(np.float32)
+        return out
+    solid = np.zeros((n, n, n), dtype=bool)            # [z, y, x]
+    t = _axes(n)
+    for a, b in edges:
+        a, b = np.asarray(a, float), np.asarray(b, float)
+        pieces = max(1, int(np.ceil(np.linalg.norm(b - a) / 0.125)))
+        for k in range(pieces):
+            pa = a + (b - a) * (k / pieces)
+            pb = a + (b - a) * ((k + 1) / pieces)
+            ab = pb - pa
+            L2 = float(ab @ ab)
+            lo, hi = np.minimum(pa, pb), np.maximum(pa, pb)
+            for ox in (-1, 0, 1):
+                for oy in (-1, 0, 1):
+                    for oz in (-1, 0, 1):
+                        o = np.array([ox, oy, oz], float)
+                        blo, bhi = lo + o - radius, hi + o + radius
+                        if np.any(bhi < 0.0) or np.any(blo > 1.0):
+                            continue
+                        # voxel index window (x, y, z) whose centres fall in the box
+                        i0 = np.clip(np.floor(blo * n - 0.5).astype(int), 0, n - 1)
+                        i1 = np.clip(np.ceil(bhi * n - 0.5).astype(int), 0, n - 1)
+                        xs, ys, zs = (t[i0[d]:i1[d] + 1] for d in range(3))
+                        P = np.stack(np.meshgrid(zs, ys, xs, indexing="ij"), axis=-1)[..., ::-1]
+                        ap = P - (pa + o)
+                        tt = np.clip((ap @ ab) / L2, 0.0, 1.0)
+                        dv = ap - tt[..., None] * ab
+                        near = np.einsum("...i,...i->...", dv, dv) <= radius * radius
+                        solid[i0[2]:i1[2] + 1, i0[1]:i1[1] + 1, i0[0]:i1[0] + 1] |= near
+    return solid.astype(np.float32)
 
 
 def shell_lattice(n: int, kind: str = "gyroid", vf: float = 0.15) -> np.ndarray:

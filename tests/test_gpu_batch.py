@@ -56,3 +56,53 @@ def test_batch_concurrent_equals_sequential_and_tensor_properties(batch):
     finally:
         for P in probs:
             P.close()
+
+
+def test_batch_graph_equals_single_problems_and_oracle():
+    """gmt_batch_*: one graph launch per V-cycle for a batch of 8 lattices
+    (truss + TPMS shells, configs[2]'s mix at 32^3) gives bitwise the
+    single-problem V-cycles; batched residual norms and C^H equal the
+    single-problem calls; one lattice's solve and C^H match the FP64 oracle
+    (App. F1, north star 1e-5)."""
+    from oracle import gmg
+    from paper_2604_26518_b200 import Batch, Problem
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mats = synth.batch_truss_psl(32, 8, seed=3)
+    A = [Problem(s, physics="elastic") for s in mats]
+    B = [Problem(s, physics="elastic") for s in mats]
+    try:
+        with Batch(B) as bt:
+            for P in A:
+                P.gmt_vcycle(3)
+            bt.gmt_batch_vcycle(3)
+            for a, b in zip(A, B):
+                assert np.array_equal(a.gmt_get_solution(), b.gmt_get_solution())
+            rb = bt.gmt_batch_residual_norms()
+            ch = bt.gmt_batch_homogenize()
+            for i, a in enumerate(A):
+                assert np.array_equal(rb[i], a.gmt_residual_norms()[0])
+                assert np.array_equal(ch[i], a.gmt_homogenize())
+            # a new material on one problem re-captures the batch graph
+            B[0].gmt_set_material(np.ascontiguousarray(mats[1], dtype=np.float32))
+            A[0].gmt_set_material(np.ascontiguousarray(mats[1], dtype=np.float32))
+            A[0].gmt_vcycle(2)
+            bt.gmt_batch_vcycle(2)
+            assert np.array_equal(A[0].gmt_get_solution(), B[0].gmt_get_solution())
+            # screening: cycle the batch to r <= 1e-5 (north star; Sec. 5.2's
+            # engineering threshold is 1e-4)
+            for _ in range(60):
+                bt.gmt_batch_vcycle(4)
+                if bt.gmt_batch_residual_norms().max() <= 1e-5:
+                    break
+            assert bt.gmt_batch_residual_norms().max() <= 1e-5
+            CH = bt.gmt_batch_homogenize()
+        ph = fem.Physics("elastic")
+        s = mats[3]
+        H = gmg.Hierarchy(s, ph, gmg.default_levels(32))
+        uo, _ = gmg.solve(H, tol=1e-9, max_cycles=400, omega=0.45, pre=2, post=2, coarse=16)
+        CHo = fem.effective_tensor(s, ph, uo)
+        assert np.abs(CH[3] - CHo).max() / np.linalg.norm(CHo) <= 1e-5
+    finally:
+        for P in A + B:
+            P.close()
