@@ -438,6 +438,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = world > 1
+    # multi-GPU: agglomerate coarse levels once a slab would hold < 8 planes
+    os.environ.setdefault("GMT_SLAB_MIN_PLANES", "8")
     if dist:
         import torch.distributed as td
         td.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -427,10 +427,16 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
 template <int DPN>
 int launch_prolong(gmt_problem p, int l, const float* e, float* u) {
   const LevelBuf &bf = p->lv[l], &bc = p->lv[l + 1];
-  const Geo g = geo(bf.n, bf.nz);
   Prof prof(p, l == 0 ? 2 : 4);
-  k_prolong_add<DPN><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n,
-                                                         l == 0 ? p->code : bf.ncode, bf.cs, bc.cs);
+  const float* act = l == 0 ? p->code : bf.ncode;
+  if (bf.nz % 2 == 0 && (bf.cs % 2) == 0) {
+    // thread per coarse cell (2 x 2 x 2 fine nodes)
+    const Geo g = geo(bc.n, bf.nz / 2);
+    k_prolong_cell<DPN><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, act, bf.cs, bc.cs);
+  } else {
+    const Geo g = geo(bf.n, bf.nz);
+    k_prolong_add<DPN><<<g.grid, g.block, 0, p->stream>>>(e, p->zm(l + 1), u, bf.n, bf.nz, bc.n, act, bf.cs, bc.cs);
+  }
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -946,8 +952,20 @@ int slab_levels(int N, int L, int P, int* Ld_out) {
   if (P == 1) { *Ld_out = 0; return GMT_OK; }
   if (N % P) return fail(GMT_ERR_ARG, "res %d not divisible by %d slabs", N, P);
   const int nz0 = N / P;
-  int Ld = 0;
-  while (Ld < L - 1 && nz0 % (1 << Ld) == 0 && (nz0 >> Ld) >= 2) ++Ld;
+  // gather level: a level stays partitioned while each slab keeps at least
+  // min_planes planes (GMT_SLAB_MIN_PLANES, default 2); coarser levels are
+  // replicated (agglomerated) on every rank.  Larger values trade a little
+  // redundant coarse work for fewer latency-bound halo exchanges of thin
+  // slabs; below 3 partitioned levels fall back to 2.
+  int min_planes = 2;
+  if (const char* v = getenv("GMT_SLAB_MIN_PLANES")) min_planes = std::max(2, atoi(v));
+  auto count = [&](int mp) {
+    int d = 0;
+    while (d < L - 1 && nz0 % (1 << d) == 0 && (nz0 >> d) >= mp) ++d;
+    return d;
+  };
+  int Ld = count(min_planes);
+  if (Ld < 3 && min_planes > 2) Ld = count(2);
   // the first replicated level Ld is assembled from every slab's region of
   // nz0 >> Ld planes: that region must be a whole number of planes (an odd
   // plane count on the last partitioned level would leave coarse planes

@@ -383,6 +383,70 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
   store_node<DPN>(u + node, csf, acc);
 }
 
+// Same operation, one thread per coarse cell (X, Y, Z): the 2 x 2 x 2 fine
+// nodes (2X + i, 2Y + j, 2Z + k) are interpolated from the cell's 8 coarse
+// corners (App. E1 weights: 1 at even, 1/2 between coarse nodes), so every
+// coarse value is read once per cell instead of once per fine node, and fine
+// rows move as float2 pairs (2X, 2X+1).  Cells whose 8 fine nodes are all
+// inactive (codes 0) are skipped.  nf even; nzf = 2 * (coarse planes).
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_prolong_cell(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int nf, int nzf, int nc,
+               const float* __restrict__ act, ptrdiff_t csf, ptrdiff_t csc) {
+  constexpr int V = Tr<DPN>::V;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z = blockIdx.z;                            // fine planes 2Z, 2Z+1
+  const bool valid = X < nc && Y < nc;
+  const ptrdiff_t pf = (ptrdiff_t)nf * nf;
+  // fine rows (j, k): base index of the pair (2X, 2X+1)
+  ptrdiff_t rowf[2][2];
+  float2 a[2][2];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      rowf[k][j] = (ptrdiff_t)(2 * Z + k) * pf + (ptrdiff_t)(2 * (valid ? Y : 0) + j) * nf + 2 * (valid ? X : 0);
+      a[k][j] = valid ? __ldg(reinterpret_cast<const float2*>(act + rowf[k][j])) : make_float2(0.f, 0.f);
+      any |= a[k][j].x != 0.f || a[k][j].y != 0.f;
+    }
+  if (!__any_sync(0xffffffffu, any) || !any) return;
+  const ptrdiff_t pc = (ptrdiff_t)nc * nc;
+  const int X1 = wrapi(X + 1, nc), Y1 = wrapi(Y + 1, nc);
+  const ptrdiff_t Z0 = (ptrdiff_t)zc(Z) * pc, Z1 = (ptrdiff_t)zc(Z + 1) * pc;
+  const ptrdiff_t c00 = (ptrdiff_t)Y * nc + X, c10 = (ptrdiff_t)Y * nc + X1;
+  const ptrdiff_t c01 = (ptrdiff_t)Y1 * nc + X, c11 = (ptrdiff_t)Y1 * nc + X1;
+#pragma unroll 3
+  for (int q = 0; q < V; ++q) {
+    const float* ec = e + q * csc;
+    // coarse corners [z][y][x]
+    float c[2][2][2];
+    c[0][0][0] = __ldg(ec + Z0 + c00); c[0][0][1] = __ldg(ec + Z0 + c10);
+    c[0][1][0] = __ldg(ec + Z0 + c01); c[0][1][1] = __ldg(ec + Z0 + c11);
+    c[1][0][0] = __ldg(ec + Z1 + c00); c[1][0][1] = __ldg(ec + Z1 + c10);
+    c[1][1][0] = __ldg(ec + Z1 + c01); c[1][1][1] = __ldg(ec + Z1 + c11);
+    float* uq = u + q * csf;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        // interpolate along z (k), then y (j): the two x-columns X, X+1
+        float col[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const float z0y0 = k ? 0.5f * (c[0][0][i] + c[1][0][i]) : c[0][0][i];
+          const float z0y1 = k ? 0.5f * (c[0][1][i] + c[1][1][i]) : c[0][1][i];
+          col[i] = j ? 0.5f * (z0y0 + z0y1) : z0y0;
+        }
+        float2 v = *reinterpret_cast<const float2*>(uq + rowf[k][j]);
+        if (a[k][j].x != 0.f) v.x += col[0];
+        if (a[k][j].y != 0.f) v.y += 0.5f * (col[0] + col[1]);
+        *reinterpret_cast<float2*>(uq + rowf[k][j]) = v;
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Coarsest level (Alg. 1 line 8): `sweeps` damped-Jacobi sweeps inside one
 // CTA (the whole coarsest grid, periodic in all axes), ping-ponging u <-> t

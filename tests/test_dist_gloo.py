@@ -80,3 +80,16 @@ def test_slab_layout_errors_and_geometry():
     with pytest.raises(GmtError):
         gmt.gmt_slab_layout(48, 4, 4, 0)
     assert gmt.gmt_slab_layout(48, 4, 2, 1) == {"z0": 24, "nz": 24, "Ld": 3, "L": 4}
+
+
+def test_gather_level_knob(monkeypatch):
+    """GMT_SLAB_MIN_PLANES: levels stay partitioned while a slab keeps that
+    many planes (512^3 on 8 ranks: 64, 32, 16, 8 planes -> 4 partitioned
+    levels instead of 6); below 3 partitioned levels the default 2 applies."""
+    from paper_2604_26518_b200 import gmt
+    monkeypatch.setenv("GMT_SLAB_MIN_PLANES", "8")
+    assert gmt.gmt_slab_layout(512, 0, 8, 3)["Ld"] == 4
+    assert gmt.gmt_slab_layout(256, 0, 8, 3)["Ld"] == 3
+    assert gmt.gmt_slab_layout(32, 4, 4, 0)["Ld"] == 3      # falls back to >= 2 planes
+    monkeypatch.delenv("GMT_SLAB_MIN_PLANES")
+    assert gmt.gmt_slab_layout(512, 0, 8, 3)["Ld"] == 6

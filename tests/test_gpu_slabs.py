@@ -175,3 +175,20 @@ def test_slabs_refinement_matches_single_device():
             assert fr <= 3e-7, (k, fr)
         CA, CB = A.gmt_homogenize(), B.gmt_homogenize()
         assert np.abs(CB - CA).max() <= 1e-6 * np.abs(CA).max()
+
+
+def test_gather_level_env_matches_single_device(monkeypatch):
+    """GMT_SLAB_MIN_PLANES moves the gather level (first replicated level):
+    64^3 on 4 slabs partitions levels 0-3 by default and 0-2 with a minimum
+    of 4 planes; both reproduce the single-device V-cycles and C^H."""
+    from paper_2604_26518_b200 import gmt
+    s = synth.tpms(64, "gyroid", 0.3)
+    monkeypatch.setenv("GMT_SLAB_MIN_PLANES", "4")
+    assert gmt.gmt_slab_layout(64, 5, 4, 0)["Ld"] == 3
+    with _problem(s, "elastic", 5) as A, _problem(s, "elastic", 5, slabs=4) as B:
+        A.gmt_vcycle(3)
+        B.gmt_vcycle(3)
+        uA, uB = A.gmt_get_solution(), B.gmt_get_solution()
+        assert np.abs(uB - uA).max() <= 1e-6 * np.abs(uA).max()
+        CA, CB = A.gmt_homogenize(), B.gmt_homogenize()
+        assert np.abs(CB - CA).max() <= 1e-6 * np.abs(CA).max()
