@@ -2,6 +2,7 @@
 // declared in include/gmt.h.  One translation unit: the kernel headers are
 // included here so every template is instantiated next to its launcher.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -152,6 +153,11 @@ struct gmt_problem_s {
   size_t cub_bytes = 0;
   int tntx = 0, tnty = 0;
   L0Consts l0c{};             // level-0 sweep constants (k_l0)
+  // TMA tensor maps of the level-0 vectors k_l0 reads (by base pointer) and of the node codes
+  struct TMap { const float* ptr; CUtensorMap map; };
+  std::vector<TMap> tmaps;
+  CUtensorMap tm_code{};
+  bool tma_ok = false;
   TcB* tcb = nullptr;         // K_e as the tf32 hi/lo B operand of the tensor-core variant (k_l0_tc)
   int l0_kernel = 0;          // 0: k_l0 (CUDA cores, default), 1: k_l0_tc (tcgen05)
   size_t bytes = 0;
@@ -319,7 +325,21 @@ dim3 tc_grid(gmt_problem p) {
 }
 template <int DPN>
 constexpr size_t l0_smem() {
-  return (size_t)L0_NB * (L0V<DPN>::NRG * DPN * L0_PLS + L0_CPL) * sizeof(float);
+  return (size_t)L0_NB * ((L0V<DPN>::NRG * DPN * L0_PLS + 31) / 32 * 32 + L0_CPL) * sizeof(float) + 128;
+}
+
+// Dynamic shared memory limit of every k_l0 instantiation (modes x rhs x tiles).
+template <int DPN>
+bool l0_attrs(int bytes) {
+  bool bad = false;
+  auto one = [&](auto k) { bad |= cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess; };
+  one(k_l0<DPN, M_JACOBI, false, L0_ALL>); one(k_l0<DPN, M_RESID, false, L0_ALL>);
+  one(k_l0<DPN, M_JACOBI, true, L0_ALL>); one(k_l0<DPN, M_RESID, true, L0_ALL>);
+  one(k_l0<DPN, M_JACOBI, false, L0_INNER>); one(k_l0<DPN, M_RESID, false, L0_INNER>);
+  one(k_l0<DPN, M_JACOBI, true, L0_INNER>); one(k_l0<DPN, M_RESID, true, L0_INNER>);
+  one(k_l0<DPN, M_JACOBI, false, L0_RING>); one(k_l0<DPN, M_RESID, false, L0_RING>);
+  one(k_l0<DPN, M_JACOBI, true, L0_RING>); one(k_l0<DPN, M_RESID, true, L0_RING>);
+  return bad;
 }
 
 template <int DPN>
@@ -355,20 +375,40 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     const dim3 grid = l0_grid<DPN>(p), block(L0_X, L0_TY);
     const size_t shm = l0_smem<DPN>();
     const float* s0 = p->s;
-    if (f) {
-      if (mode == M_JACOBI)
-        k_l0<DPN, M_JACOBI, true><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
-                                                             p->tflag, p->tntx, p->tnty, f);
-      else
-        k_l0<DPN, M_RESID, true><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
-                                                            p->tflag, p->tntx, p->tnty, f);
+    const CUtensorMap* tmu = nullptr;
+    if (p->tma_ok && !getenv("GMT_NO_TMA"))
+      for (const auto& t : p->tmaps)
+        if (t.ptr == u) tmu = &t.map;
+    const int zg = b.gh;
+    const int ntx8 = (int)grid.x, nty8 = (int)grid.y;
+    auto go = [&](auto tl, dim3 g, double* pt) {
+      constexpr int TL = decltype(tl)::value;
+      const CUtensorMap& tm = tmu ? *tmu : p->tm_code;
+      if (f) {
+        if (mode == M_JACOBI)
+          k_l0<DPN, M_JACOBI, true, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
+                                                               p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg);
+        else
+          k_l0<DPN, M_RESID, true, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
+                                                              p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg);
+      } else {
+        if (mode == M_JACOBI)
+          k_l0<DPN, M_JACOBI, false, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
+                                                                p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg);
+        else
+          k_l0<DPN, M_RESID, false, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
+                                                               p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg);
+      }
+    };
+    if (tmu && ntx8 >= 3 && nty8 >= 3) {
+      // interior tiles staged by TMA, then the ring of boundary tiles by cp.async
+      const dim3 gi(ntx8 - 2, nty8 - 2, grid.z), gr(2 * ntx8 + 2 * (nty8 - 2), 1, grid.z);
+      go(std::integral_constant<int, L0_INNER>{}, gi, part);
+      LAUNCHED(p);
+      go(std::integral_constant<int, L0_RING>{}, gr,
+         part ? part + (size_t)gi.x * gi.y * gi.z * 2 * Tr<DPN>::NR : nullptr);
     } else {
-      if (mode == M_JACOBI)
-        k_l0<DPN, M_JACOBI, false><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
-                                                              p->tflag, p->tntx, p->tnty, nullptr);
-      else
-        k_l0<DPN, M_RESID, false><<<grid, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, part, cs,
-                                                             p->tflag, p->tntx, p->tnty, nullptr);
+      go(std::integral_constant<int, L0_ALL>{}, grid, part);
     }
   } else if (l == 0) {
     const ZMap z = p->zm(0);
@@ -762,6 +802,8 @@ int residual_norms(gmt_problem p, double* rel, double* ar, double* af) {
 
 // ---- mixed-precision iterative refinement (level 0)
 
+int l0_tma_add(gmt_problem p, const float* vec);
+
 int refine_alloc(gmt_problem p) {
   LevelBuf& b = p->lv[0];
   const ptrdiff_t goff = (ptrdiff_t)b.gh * b.n * b.n;
@@ -770,6 +812,7 @@ int refine_alloc(gmt_problem p) {
       TRY(dalloc(p, (void**)v, vbytes(p, b)));
       *v += goff;
       CK(cudaMemsetAsync(vbase(b, *v), 0, vbytes(p, b), p->stream));
+      if (*v != p->f0) TRY(l0_tma_add(p, *v));   // refinement defect passes read hi and lo
     }
   return GMT_OK;
 }
@@ -891,6 +934,66 @@ int check_level(gmt_problem p, int level, bool allow_coarsest = true) {
   if (p->grp) return fail(GMT_ERR_STATE, "row-level entry points act on single-device problems only");
   if (level < 0 || level >= p->L || (!allow_coarsest && level >= p->L - 1))
     return fail(GMT_ERR_ARG, "level %d out of range (L=%d)", level, p->L);
+  return GMT_OK;
+}
+
+// TMA tensor maps for k_l0 (interior tiles): 4-D [V][nz + 2 gh][n][n] view of
+// a level-0 vector (box [NRG*DPN][10][40], the ring-slot layout) and 3-D
+// [nz + 2][n][n] of the node codes (box [8][32]).  Needs n % 4 == 0 (16-byte
+// strides); otherwise k_l0 stages with cp.async everywhere.
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+int l0_tma_add(gmt_problem p, const float* vec) {
+  if (!p->tma_ok || !vec) return GMT_OK;
+  const LevelBuf& b = p->lv[0];
+  auto enc = tma_encode_fn();
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {(cuuint64_t)b.n, (cuuint64_t)b.n, (cuuint64_t)(b.nz + 2 * b.gh), (cuuint64_t)p->V};
+  const cuuint64_t strides[3] = {(cuuint64_t)b.n * 4, (cuuint64_t)b.n * b.n * 4, (cuuint64_t)b.cs * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)(L0_X + 8), (cuuint32_t)L0_PY, 1u, (cuuint32_t)(p->dpn == 3 ? 6 : 1)};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)(vec - (ptrdiff_t)b.gh * b.n * b.n), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    p->tma_ok = false;
+    return GMT_OK;
+  }
+  for (auto& t : p->tmaps)
+    if (t.ptr == vec) { t.map = m; return GMT_OK; }
+  p->tmaps.push_back({vec, m});
+  return GMT_OK;
+}
+
+int l0_tma_setup(gmt_problem p) {
+  const LevelBuf& b = p->lv[0];
+  p->tma_ok = tma_encode_fn() != nullptr && b.n % 4 == 0 && b.n >= 64;
+  if (!p->tma_ok) return GMT_OK;
+  const cuuint64_t dims[3] = {(cuuint64_t)b.n, (cuuint64_t)b.n, (cuuint64_t)(b.nz + 2)};
+  const cuuint64_t strides[2] = {(cuuint64_t)b.n * 4, (cuuint64_t)b.n * b.n * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)L0_X, (cuuint32_t)L0_Y, 1u};
+  const cuuint32_t es[3] = {1, 1, 1};
+  if (tma_encode_fn()(&p->tm_code, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)(p->code - (ptrdiff_t)b.n * b.n), dims,
+                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    p->tma_ok = false;
+    return GMT_OK;
+  }
+  TRY(l0_tma_add(p, b.u));
+  TRY(l0_tma_add(p, b.t));
   return GMT_OK;
 }
 
@@ -1170,14 +1273,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_coarse_tiled<3, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm3) ||
         cudaFuncSetAttribute(k_coarse_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_coarse_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
-        cudaFuncSetAttribute(k_l0<3, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
-        cudaFuncSetAttribute(k_l0<3, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
-        cudaFuncSetAttribute(k_l0<3, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
-        cudaFuncSetAttribute(k_l0<3, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l3) ||
-        cudaFuncSetAttribute(k_l0<1, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
-        cudaFuncSetAttribute(k_l0<1, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
-        cudaFuncSetAttribute(k_l0<1, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
-        cudaFuncSetAttribute(k_l0<1, M_RESID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, l1) ||
+        l0_attrs<3>(l3) || l0_attrs<1>(l1) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
@@ -1249,6 +1345,7 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
     cudaError_t e = cudaGetLastError();
     return bail(fail(GMT_ERR_CUDA, "allocation failed: %s", cudaGetErrorString(e)));
   }
+  if ((rc = l0_tma_setup(p)) != GMT_OK) return bail(rc);
   *out = p;
   return GMT_OK;
 }

@@ -40,6 +40,8 @@
 // update.  Void nodes (code 0) carry no unknowns and are not written.
 #pragma once
 
+#include <cuda.h>
+
 #include "f32x2.cuh"
 #include "gmt_common.cuh"
 #include "k_level.cuh"
@@ -127,6 +129,38 @@ __device__ __forceinline__ void l0_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void l0_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// TMA (cp.async.bulk.tensor) staging with one mbarrier per ring slot.
+__device__ __forceinline__ uint32_t l0_s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void l0_mbar_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(l0_s32(m)));
+}
+__device__ __forceinline__ void l0_mbar_expect(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(l0_s32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void l0_mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "L0W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra L0W_%=;\n\t}\n" ::"r"(l0_s32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void l0_tma4(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3, uint64_t* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+          l0_s32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(l0_s32(m))
+      : "memory");
+}
+__device__ __forceinline__ void l0_tma3(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          l0_s32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(l0_s32(m))
+      : "memory");
+}
+
 // Sign of unit-strain load case m under the reflections of the axes r with
 // t_r = -1 (App. F1 order 11, 22, 33, 23, 13, 12; heat: gradient e_m).
 template <int DPN>
@@ -139,19 +173,30 @@ __device__ __forceinline__ float l0_tau(int m, float tx, float ty, float tz) {
 // FEXP: f read from f_all (iterative refinement defect) instead of the element
 // loads.  blockIdx.z = z-chunk * NG + load-case group.  part (optional): per
 // CTA 2 * NR doubles, sum r^2 then sum f^2 per load case.
-template <int DPN, int MODE, bool FEXP>
+// TL selects the tiles of the launch: L0_ALL (every tile, cp.async staging),
+// L0_INNER (tiles whose staged box lies inside the grid: TMA staging, grid
+// (ntx - 2) x (nty - 2)), L0_RING (the remaining tiles, cp.async; grid.x
+// enumerates the ring of boundary tiles).
+constexpr int L0_ALL = 0, L0_INNER = 1, L0_RING = 2;
+template <int DPN, int MODE, bool FEXP, int TL = L0_ALL>
 __global__ void __launch_bounds__(L0_NTH, 3)
 k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, ZMap zu,
      float* __restrict__ out_all, int n, int nz, const L0Consts C, double* __restrict__ part, ptrdiff_t cs,
-     const uint8_t* __restrict__ flag, int ntx, int nty4, const float* __restrict__ f_all) {
+     const uint8_t* __restrict__ flag, int ntx, int nty4, const float* __restrict__ f_all,
+     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_code, int zg) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "level-0 sweep: V-cycle modes only");
   using V = L0V<DPN>;
   using T = typename V::T;
   constexpr int NR = Tr<DPN>::NR, NRG = V::NRG, NG = NR / NRG, VG = NRG * DPN;
-  constexpr int SLOT = VG * L0_PLS;        // floats per ring slot of u
+  constexpr int SLOT = (VG * L0_PLS + 31) / 32 * 32;   // floats per ring slot of u (128-byte aligned)
   constexpr int LCS = DPN * L0_PLS;        // smem distance between the group's load cases
   constexpr int NW = L0_NTH / 32;
-  extern __shared__ __align__(16) float smem[];   // [L0_NB][VG][L0_PY][L0_RS], then codes [L0_NB][L0_Y][L0_X]
+  // [L0_NB][VG][L0_PY][L0_RS] (128-byte aligned slots, the TMA box layout), then codes [L0_NB][L0_Y][L0_X].
+  // The dynamic window follows the static shared variables (16-byte aligned):
+  // advance to the next 128-byte boundary by integer offset, which keeps the
+  // pointer in the shared address space (plain LDS / STS).
+  extern __shared__ __align__(16) float smem_dyn[];
+  float* const smem = smem_dyn + ((32u - ((uint32_t)__cvta_generic_to_shared(smem_dyn) >> 2)) & 31u);
   float* const cring = smem + L0_NB * SLOT;
   // interface nodes of a completed target plane, per warp (double-buffered by
   // the plane's parity: written in the iteration that completes the plane,
@@ -168,7 +213,24 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
 
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * L0_X + tx;
   const int lane = tid & 31, warp = tid >> 5;
-  const int x0 = blockIdx.x * L0_X, y0 = blockIdx.y * L0_Y;
+  // tile of this CTA
+  int bx = blockIdx.x, by = blockIdx.y;
+  const int ntx8 = (n + L0_X - 1) / L0_X, nty8 = (n + L0_Y - 1) / L0_Y;
+  if (TL == L0_INNER) {
+    bx += 1;
+    by += 1;
+  } else if (TL == L0_RING) {                   // rows 0 and nty8-1, then columns 0 and ntx8-1
+    const int i = blockIdx.x;
+    if (i < 2 * ntx8) {
+      bx = i % ntx8;
+      by = i < ntx8 ? 0 : nty8 - 1;
+    } else {
+      const int j = i - 2 * ntx8;
+      bx = (j & 1) ? ntx8 - 1 : 0;
+      by = 1 + (j >> 1);
+    }
+  }
+  const int x0 = bx * L0_X, y0 = by * L0_Y;
   const int z0 = chunk * L0_ZC, z1 = min(nz, z0 + L0_ZC);
   const int x = x0 + tx, ya = y0 + 2 * ty;      // nodes (x, ya) and (x, ya + 1)
   const bool va = x < n && ya < n, vb = x < n && ya + 1 < n;
@@ -180,9 +242,9 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
   static_assert(L0_ZC + 5 <= 64, "flag window");
   auto tflag = [&](int zv) -> bool {
     const ptrdiff_t r = (ptrdiff_t)zs(zv) * nty4;
-    const int t4 = 2 * blockIdx.y;
-    bool a = flag[(r + t4) * ntx + blockIdx.x] != 0;
-    if (t4 + 1 < nty4) a |= flag[(r + t4 + 1) * ntx + blockIdx.x] != 0;
+    const int t4 = 2 * by;
+    bool a = flag[(r + t4) * ntx + bx] != 0;
+    if (t4 + 1 < nty4) a |= flag[(r + t4 + 1) * ntx + bx] != 0;
     return a;
   };
   unsigned long long fm = __ballot_sync(0xffffffffu, tflag(z0 - 3 + lane));
@@ -271,15 +333,44 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
   // ring slots: plane pl lives in slot (pl - (z0 - 1)) mod NB
   int sl_p = 0;                                         // slot of plane p
   auto sl_add = [&](int a, int d) -> int { const int r = a + d; return r >= L0_NB ? r - L0_NB : (r < 0 ? r + L0_NB : r); };
-  // prologue: u planes z0-1, z0; codes z0-1 .. z0+1
-  if ((F & 0xf) != 0) issue_u(z0 - 1, 0);
-  issue_code(z0 - 1, 0);
-  issue_code(z0, 1);
-  if (z0 + 1 <= z1) issue_code(z0 + 1, 2);
-  l0_commit();
-  if (((F >> 1) & 0xf) != 0) issue_u(z0, 1);
-  if (z0 + 2 <= z1) issue_code(z0 + 2, 3);
-  l0_commit();
+
+  // Interior tiles (the staged box x0-4 .. x0+35, y0-1 .. y0+8 inside the
+  // grid, no periodic wrap) stage through TMA: one elected thread issues a
+  // 4-D box [VG][10][40] of u (exactly the slot layout) and the 32 x 8 code
+  // box, completing on the slot's mbarrier; boundary tiles (and grids whose
+  // strides TMA cannot describe) use the cp.async path.
+  constexpr bool tma = TL == L0_INNER;
+  __shared__ __align__(8) uint64_t s_mbar[L0_NB];
+  uint32_t phase_bits = 0;                              // TMA: parity of each slot's next completion
+  if (tma) {
+    if (tid == 0) {
+#pragma unroll
+      for (int i = 0; i < L0_NB; ++i) l0_mbar_init(&s_mbar[i]);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  constexpr uint32_t UBYTES = VG * L0_PLS * 4, CBYTES = L0_CPL * 4;
+  // stage into slot sl (which holds plane psl): u of psl when want_u, and the
+  // codes of planes c0..c1 into their own code slots; one completion per call
+  auto stage = [&](int sl, int psl, bool want_u, int c0, int c1) {
+    if (tma) {
+      if (tid == 0) {
+        const int ncode = c1 >= c0 ? c1 - c0 + 1 : 0;
+        l0_mbar_expect(&s_mbar[sl], (want_u ? UBYTES : 0u) + ncode * CBYTES);
+        if (want_u) l0_tma4(smem + sl * SLOT, &tm_u, x0 - 4, y0 - 1, zu(psl) + zg, m0 * DPN, &s_mbar[sl]);
+        for (int c = c0; c <= c1; ++c)
+          l0_tma3(cring + sl_add(sl, c - psl) * L0_CPL, &tm_code, x0, y0, c + 1, &s_mbar[sl]);
+      }
+    } else {
+      if (want_u) issue_u(psl, sl);
+      for (int c = c0; c <= c1; ++c) issue_code(c, sl_add(sl, c - psl));
+      l0_commit();
+    }
+  };
+  // prologue: u planes z0-1, z0; codes z0-1 .. z0+2
+  stage(0, z0 - 1, (F & 0xf) != 0, z0 - 1, min(z0 + 1, z1));
+  stage(1, z0, ((F >> 1) & 0xf) != 0, z0 + 2, min(z0 + 2, z1));
 
   const int ca_off = 2 * ty * L0_X + tx;               // own node a in a code plane
   float ca_prev = 0.f, cb_prev = 0.f;                  // codes of plane p-1 (nodes a, b)
@@ -291,13 +382,19 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
   // unroll by 3 that rotates the roles instead of the registers measured
   // slower: the triplicated interface path overflows the instruction cache.)
   for (int p = z0 - 1; p <= z1 + 1; ++p) {
-    if (p <= z1) l0_wait<L0_AHEAD - 1>();
+    if (p <= z1) {
+      if (tma) {
+        l0_mbar_wait(&s_mbar[sl_p], (phase_bits >> sl_p) & 1u);
+        phase_bits ^= 1u << sl_p;
+      } else {
+        l0_wait<L0_AHEAD - 1>();
+      }
+    }
     __syncthreads();   // plane p staged; iteration p-1 done: its ring slot and interface list are free
     {
       const int pl = p + L0_AHEAD, sl = sl_add(sl_p, L0_AHEAD);
-      if (pl <= z1 && ((F >> L0_AHEAD) & 0xf) != 0) issue_u(pl, sl);
-      if (pl + 1 <= z1) issue_code(pl + 1, sl_add(sl, 1));
-      l0_commit();
+      if (pl <= z1) stage(sl, pl, ((F >> L0_AHEAD) & 0xf) != 0, pl + 1, min(pl + 1, z1));
+      else if (!tma) l0_commit();
     }
     if (first) {
       first = false;

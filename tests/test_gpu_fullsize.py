@@ -161,3 +161,34 @@ def test_effective_tensor_of_given_field(n, slabs):
     want /= float(n) ** 3
     err = np.abs(CH - want).max() / np.linalg.norm(want)
     assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("kind", ["elastic", "thermal"])
+def test_tma_staging_equals_cp_async(kind, monkeypatch):
+    """k_l0 stages interior tiles by TMA (cp.async.bulk.tensor) and boundary
+    tiles by cp.async: with TMA switched off (GMT_NO_TMA) the staged values,
+    hence the sweep, are bitwise the same (256^3 gyroid, one level, one sweep;
+    plus a full V-cycle of the 4-level hierarchy)."""
+    from paper_2604_26518_b200 import Problem
+    n = 256
+    s = synth.tpms(n, "gyroid", 0.3)
+    ph = fem.Physics(kind)
+    om = OMEGA if kind == "elastic" else 0.6
+    u0 = synth.initial_guess(n, ph.nrhs, ph.dpn, seed=2, material=s)
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("GMT_NO_TMA", env)
+        else:
+            monkeypatch.delenv("GMT_NO_TMA", raising=False)
+        with Problem(s, physics=kind, levels=1, coarse_sweeps=1, omega=om) as P:
+            P.gmt_set_initial_guess(u0)
+            P.gmt_vcycle(1)
+            a = P.gmt_get_solution()
+        with Problem(s, physics=kind, levels=4, omega=om) as P:
+            P.gmt_set_initial_guess(u0)
+            P.gmt_vcycle(1)
+            b = P.gmt_get_solution()
+        outs.append((a, b))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
