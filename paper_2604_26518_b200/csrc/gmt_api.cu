@@ -119,6 +119,11 @@ struct gmt_problem_s {
   // of the Galerkin build (ordered after the solution reset by ev_u_ready)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_u_ready = nullptr, ev_copy = nullptr;
+  // a second compute stream: launches of one sweep that touch disjoint nodes
+  // (level-0 interior / boundary tiles, coarse uniform / interface nodes) run
+  // as parallel branches (fork / join events; parallel nodes in the graph)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool u_ready_pending = false;
   // level-0 solution reset deferred by gmt_set_material until the next public
   // call (set_device): a following gmt_set_initial_guess overwrites it anyway
@@ -328,6 +333,19 @@ constexpr size_t l0_smem() {
   return (size_t)L0_NB * ((L0V<DPN>::NRG * DPN * L0_PLS + 31) / 32 * 32 + L0_CPL) * sizeof(float) + 128;
 }
 
+// Fork: work enqueued on p->aux after this runs after everything already on
+// p->stream; join: p->stream waits for it.
+int aux_fork(gmt_problem p) {
+  CK(cudaEventRecord(p->ev_fork, p->stream));
+  CK(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+  return GMT_OK;
+}
+int aux_join(gmt_problem p) {
+  CK(cudaEventRecord(p->ev_join, p->aux));
+  CK(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
+  return GMT_OK;
+}
+
 // Dynamic shared memory limit of every k_l0 instantiation (modes x rhs x tiles).
 template <int DPN>
 bool l0_attrs(int bytes) {
@@ -381,7 +399,7 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
         if (t.ptr == u) tmu = &t.map;
     const int zg = b.gh;
     const int ntx8 = (int)grid.x, nty8 = (int)grid.y;
-    auto go = [&](auto tl, dim3 g, double* pt) {
+    auto go = [&](auto tl, dim3 g, double* pt, cudaStream_t st) {
       constexpr int TL = decltype(tl)::value;
       const CUtensorMap& tm = tmu ? *tmu : p->tm_code;
       if (f) {
@@ -400,15 +418,21 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
                                                                p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg);
       }
     };
-    if (tmu && ntx8 >= 3 && nty8 >= 3) {
+    // the split pays when interior tiles dominate (>= 256 nodes across)
+    if (tmu && b.n >= 256) {
       // interior tiles staged by TMA, then the ring of boundary tiles by cp.async
       const dim3 gi(ntx8 - 2, nty8 - 2, grid.z), gr(2 * ntx8 + 2 * (nty8 - 2), 1, grid.z);
-      go(std::integral_constant<int, L0_INNER>{}, gi, part);
+      // (disjoint nodes: the ring runs as a parallel branch on the aux stream)
+      TRY(aux_fork(p));
+      go(std::integral_constant<int, L0_INNER>{}, gi, part, st);
       LAUNCHED(p);
       go(std::integral_constant<int, L0_RING>{}, gr,
-         part ? part + (size_t)gi.x * gi.y * gi.z * 2 * Tr<DPN>::NR : nullptr);
+         part ? part + (size_t)gi.x * gi.y * gi.z * 2 * Tr<DPN>::NR : nullptr, p->aux);
+      LAUNCHED(p);
+      TRY(aux_join(p));
+      return GMT_OK;
     } else {
-      go(std::integral_constant<int, L0_ALL>{}, grid, part);
+      go(std::integral_constant<int, L0_ALL>{}, grid, part, st);
     }
   } else if (l == 0) {
     const ZMap z = p->zm(0);
@@ -424,6 +448,11 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     const ZMap z = p->zm(l);
     const dim3 grid(b.tntx, b.tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * (Tr<DPN>::NR / 3)), block(TT_X, TT_Y);
     const size_t shm = (size_t)TT_NB * 3 * DPN * TT_PLS * sizeof(float);
+    // uniform nodes (tiled) and interface nodes (list) are disjoint: the
+    // interface kernel runs as a parallel branch on the aux stream
+    static const int aux_min = getenv("GMT_AUX_COARSE_MIN") ? atoi(getenv("GMT_AUX_COARSE_MIN")) : (1 << 30);
+    const bool split = b.icount > 0 && b.n >= aux_min;
+    if (split) TRY(aux_fork(p));
     if (mode == M_JACOBI)
       k_coarse_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, om, cs, b.tflag,
                                                                  b.tntx, b.tnty, f, p->hc[l]);
@@ -433,10 +462,14 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     LAUNCHED(p);
     if (b.icount == 0) return GMT_OK;
     const int nbi = (b.icount + 127) / 128;
+    cudaStream_t si = split ? p->aux : st;
     if (mode == M_JACOBI)
-      k_coarse_iface<DPN, M_JACOBI><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_JACOBI><<<nbi, 128, 0, si>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
     else
-      k_coarse_iface<DPN, M_RESID><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_RESID><<<nbi, 128, 0, si>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+    LAUNCHED(p);
+    if (split) TRY(aux_join(p));
+    return GMT_OK;
   } else {
     const ZMap z = p->zm(l);
     switch (mode) {
@@ -459,8 +492,7 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
   const float* sd = skip_void ? bc.ncode : nullptr;
   const float* actf = l == 0 ? p->code : bf.ncode;
   k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
-                                                      bf.cs, bc.cs, actf);
-  LAUNCHED(p);
+                                                      bf.cs, bc.cs, actf);  LAUNCHED(p);
   return GMT_OK;
 }
 
@@ -920,6 +952,9 @@ void free_all(gmt_problem p) {
   if (p->code) cudaFree(p->code - (size_t)p->N * p->N); cudaFree(p->elist); cudaFree(p->alist); cudaFree(p->l2list); cudaFree(p->eflag); cudaFree(p->icount_d); cudaFree(p->cub_tmp); cudaFree(p->part); cudaFree(p->red); cudaFree(p->u8tmp);
   if (p->hred) cudaFreeHost(p->hred);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->aux) cudaStreamDestroy(p->aux);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->ev_u_ready) cudaEventDestroy(p->ev_u_ready);
   if (p->ev_copy) cudaEventDestroy(p->ev_copy);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
@@ -1165,6 +1200,10 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
       return bail(fail(GMT_ERR_CUDA, "cudaStreamCreate failed"));
     p->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(GMT_ERR_CUDA, "aux stream / event creation failed"));
   if (cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_u_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_copy, cudaEventDisableTiming) != cudaSuccess)

@@ -48,8 +48,8 @@
 
 namespace gmt {
 
-constexpr int L0_X = 32, L0_Y = 8, L0_ZC = 32, L0_NB = 6, L0_AHEAD = 2;
-static_assert(L0_NB >= L0_AHEAD + 4, "ring: planes p-3 .. p+AHEAD resident");
+constexpr int L0_X = 32, L0_Y = 8, L0_ZC = 32, L0_NB = 5, L0_AHEAD = 1;
+static_assert(L0_NB >= L0_AHEAD + 4, "ring: planes p-3 .. p+AHEAD resident (interface pass of plane p-2)");
 constexpr int L0_TY = L0_Y / 2;            // thread rows: each thread owns 2 nodes of a column (y, y+1)
 constexpr int L0_RS = 40;                  // smem row stride: halo-left at 3, interior 4..35, halo-right 36
 constexpr int L0_PY = L0_Y + 2;
@@ -179,7 +179,7 @@ __device__ __forceinline__ float l0_tau(int m, float tx, float ty, float tz) {
 // enumerates the ring of boundary tiles).
 constexpr int L0_ALL = 0, L0_INNER = 1, L0_RING = 2;
 template <int DPN, int MODE, bool FEXP, int TL = L0_ALL>
-__global__ void __launch_bounds__(L0_NTH, 3)
+__global__ void __launch_bounds__(L0_NTH, 4)
 k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, ZMap zu,
      float* __restrict__ out_all, int n, int nz, const L0Consts C, double* __restrict__ part, ptrdiff_t cs,
      const uint8_t* __restrict__ flag, int ntx, int nty4, const float* __restrict__ f_all,
@@ -368,9 +368,12 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
       l0_commit();
     }
   };
-  // prologue: u planes z0-1, z0; codes z0-1 .. z0+2
-  stage(0, z0 - 1, (F & 0xf) != 0, z0 - 1, min(z0 + 1, z1));
-  stage(1, z0, ((F >> 1) & 0xf) != 0, z0 + 2, min(z0 + 2, z1));
+  // prologue: u planes z0-1 .. z0-2+AHEAD; with them the codes up to plane
+  // z0-1+AHEAD (iteration p needs the codes of planes <= p+1; the stage
+  // issued in iteration p brings those of plane p+AHEAD+1)
+#pragma unroll
+  for (int i = 0; i < L0_AHEAD; ++i)
+    stage(i, z0 - 1 + i, ((F >> i) & 0xf) != 0, i == 0 ? z0 - 1 : z0 + i, min(z0 + i, z1));
 
   const int ca_off = 2 * ty * L0_X + tx;               // own node a in a code plane
   float ca_prev = 0.f, cb_prev = 0.f;                  // codes of plane p-1 (nodes a, b)
