@@ -492,7 +492,8 @@ int launch_restrict(gmt_problem p, int l, const float* r, float* fc, bool skip_v
   const float* sd = skip_void ? bc.ncode : nullptr;
   const float* actf = l == 0 ? p->code : bf.ncode;
   k_restrict<DPN><<<g.grid, g.block, 0, p->stream>>>(r, p->zm(l), fc, bc.n, bc.nz, bf.n, sd,
-                                                      bf.cs, bc.cs, actf);  LAUNCHED(p);
+                                                      bf.cs, bc.cs, actf);
+  LAUNCHED(p);
   return GMT_OK;
 }
 
