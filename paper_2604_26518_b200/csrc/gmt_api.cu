@@ -1000,7 +1000,7 @@ int l0_tma_add(gmt_problem p, const float* vec) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {(cuuint64_t)b.n, (cuuint64_t)b.n, (cuuint64_t)(b.nz + 2 * b.gh), (cuuint64_t)p->V};
   const cuuint64_t strides[3] = {(cuuint64_t)b.n * 4, (cuuint64_t)b.n * b.n * 4, (cuuint64_t)b.cs * 4};
-  const cuuint32_t box[4] = {(cuuint32_t)(L0_X + 8), (cuuint32_t)L0_PY, 1u, (cuuint32_t)(p->dpn == 3 ? 6 : 1)};
+  const cuuint32_t box[4] = {(cuuint32_t)(L0_X + 8), (cuuint32_t)L0_PY, 1u, (cuuint32_t)(p->dpn == 3 ? 6 : 3)};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)(vec - (ptrdiff_t)b.gh * b.n * b.n), dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

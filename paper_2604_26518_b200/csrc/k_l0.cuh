@@ -7,7 +7,7 @@
 //
 // Work decomposition.  A CTA owns a L0_X x L0_Y column of nodes, a chunk of
 // L0_ZC node planes and one group of load cases (elasticity: two load cases
-// packed into f32x2 lanes, three groups; heat: one load case, three groups);
+// packed into f32x2 lanes, three groups; heat: all three load cases);
 // each thread owns two y-adjacent nodes, which share two of the four staged
 // rows they read.  The CTA marches up the chunk; node planes of u (one-node
 // halo, periodic wrap) and of the node codes are staged into a ring of
@@ -85,6 +85,7 @@ template <> struct L0V<3> {      // elasticity: load cases (2g, 2g+1) in the two
   static constexpr int NRG = 2;
   __device__ static __forceinline__ T splat(float a) { return pk2(a, a); }
   __device__ static __forceinline__ T zero() { return 0ull; }
+  __device__ static __forceinline__ T make(const float (&v)[2]) { return pk2(v[0], v[1]); }
   // component record of load case 0 at p, load case 1 at p + lcs
   __device__ static __forceinline__ T ld(const float* p, int lcs) { return pk2(p[0], p[lcs]); }
   __device__ static __forceinline__ T ldg(const float* p, ptrdiff_t lcs) { return pk2(__ldg(p), __ldg(p + lcs)); }
@@ -105,16 +106,34 @@ template <> struct L0V<3> {      // elasticity: load cases (2g, 2g+1) in the two
     return pk2(__shfl_xor_sync(0xffffffffu, a, m), __shfl_xor_sync(0xffffffffu, b, m));
   }
 };
-template <> struct L0V<1> {      // heat: one load case per group
-  using T = float;
-  static constexpr int NRG = 1;
-  __device__ static __forceinline__ T splat(float a) { return a; }
-  __device__ static __forceinline__ T zero() { return 0.f; }
-  __device__ static __forceinline__ T ld(const float* p, int) { return p[0]; }
-  __device__ static __forceinline__ T ldg(const float* p, ptrdiff_t) { return __ldg(p); }
-  __device__ static __forceinline__ void st(float* p, ptrdiff_t, T v) { p[0] = v; }
-  __device__ static __forceinline__ float lane(T v, int) { return v; }
-  __device__ static __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+// heat: the three load cases of a node in one CTA, as a 3-wide scalar value
+struct f3 {
+  float a, b, c;
+};
+__device__ __forceinline__ f3 vadd(f3 x, f3 y) { return {x.a + y.a, x.b + y.b, x.c + y.c}; }
+__device__ __forceinline__ f3 vsub(f3 x, f3 y) { return {x.a - y.a, x.b - y.b, x.c - y.c}; }
+__device__ __forceinline__ f3 vmul(f3 x, f3 y) { return {x.a * y.a, x.b * y.b, x.c * y.c}; }
+__device__ __forceinline__ f3 vfma(f3 x, f3 y, f3 z) { return {fmaf(x.a, y.a, z.a), fmaf(x.b, y.b, z.b), fmaf(x.c, y.c, z.c)}; }
+template <> struct L0V<1> {      // heat: load cases 0, 1, 2 in the three members
+  using T = f3;
+  static constexpr int NRG = 3;
+  __device__ static __forceinline__ T splat(float a) { return {a, a, a}; }
+  __device__ static __forceinline__ T zero() { return {0.f, 0.f, 0.f}; }
+  __device__ static __forceinline__ T make(const float (&v)[3]) { return {v[0], v[1], v[2]}; }
+  __device__ static __forceinline__ T ld(const float* p, int lcs) { return {p[0], p[lcs], p[2 * lcs]}; }
+  __device__ static __forceinline__ T ldg(const float* p, ptrdiff_t lcs) {
+    return {__ldg(p), __ldg(p + lcs), __ldg(p + 2 * lcs)};
+  }
+  __device__ static __forceinline__ void st(float* p, ptrdiff_t lcs, T v) {
+    p[0] = v.a;
+    p[lcs] = v.b;
+    p[2 * lcs] = v.c;
+  }
+  __device__ static __forceinline__ float lane(T v, int j) { return j == 0 ? v.a : (j == 1 ? v.b : v.c); }
+  __device__ static __forceinline__ T shfl_xor(T v, int m) {
+    return {__shfl_xor_sync(0xffffffffu, v.a, m), __shfl_xor_sync(0xffffffffu, v.b, m),
+            __shfl_xor_sync(0xffffffffu, v.c, m)};
+  }
 };
 
 __device__ __forceinline__ void l0_cp4(float* smem, const float* gmem) {
@@ -196,7 +215,8 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
   // advance to the next 128-byte boundary by integer offset, which keeps the
   // pointer in the shared address space (plain LDS / STS).
   extern __shared__ __align__(16) float smem_dyn[];
-  float* const smem = smem_dyn + ((32u - ((uint32_t)__cvta_generic_to_shared(smem_dyn) >> 2)) & 31u);
+  float* const smem =
+      TL == L0_INNER ? smem_dyn + ((32u - ((uint32_t)__cvta_generic_to_shared(smem_dyn) >> 2)) & 31u) : smem_dyn;
   float* const cring = smem + L0_NB * SLOT;
   // interface nodes of a completed target plane, per warp (double-buffered by
   // the plane's parity: written in the iteration that completes the plane,
@@ -622,10 +642,7 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
               float fl[NRG];
 #pragma unroll
               for (int jj = 0; jj < NRG; ++jj) fl[jj] = sp * l0_tau<DPN>(m0 + jj, tX, tY, tZ) * C.F0[pp * NR + m0 + jj];
-              T fv;
-              if constexpr (NRG == 2) fv = pk2(fl[0], fl[1]);
-              else fv = fl[0];
-              facc[pp] = fv;
+              facc[pp] = V::make(fl);
             }
           }
         }

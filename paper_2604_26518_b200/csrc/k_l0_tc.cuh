@@ -56,6 +56,7 @@ k_l0_tc(const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, Z
         const float* __restrict__ f_all) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "level-0 sweep: V-cycle modes only");
   constexpr int NR = Tr<DPN>::NR, NRG = L0V<DPN>::NRG, NG = NR / NRG, VG = NRG * DPN, ND = 8 * DPN;
+  constexpr int TCOLS = NRG <= 2 ? 64 : 128;    // TMEM columns: 32 per load case, power of 2
   static_assert(ND <= TC_K, "element dofs");
   extern __shared__ __align__(1024) unsigned char tsm[];
   float* ring = reinterpret_cast<float*>(tsm);                                  // [NB][VG][PP]
@@ -85,7 +86,7 @@ k_l0_tc(const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, Z
     Bs[o] = Bop->hi[i];
     Bs[TC_N * TC_K + o] = Bop->lo[i];
   }
-  if (warp == 0) tc::tmem_alloc<64>(&taddr_s);
+  if (warp == 0) tc::tmem_alloc<TCOLS>(&taddr_s);
   if (tid == 0) {
     tc::mbar_init(&mbar, 1);
     tc::fence_mbar_init();
@@ -290,7 +291,7 @@ k_l0_tc(const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, Z
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (warp == 0) tc::tmem_free<64>(taddr);
+  if (warp == 0) tc::tmem_free<TCOLS>(taddr);
   if (part) {
     __shared__ double s_nr[2 * NRG];
     block_reduce_store<2 * NRG>(nrm, s_nr);
