@@ -49,6 +49,7 @@
 namespace gmt {
 
 constexpr int L0_X = 32, L0_Y = 8, L0_ZC = 32, L0_NB = 5, L0_AHEAD = 1;
+
 static_assert(L0_NB >= L0_AHEAD + 4, "ring: planes p-3 .. p+AHEAD resident (interface pass of plane p-2)");
 constexpr int L0_TY = L0_Y / 2;            // thread rows: each thread owns 2 nodes of a column (y, y+1)
 constexpr int L0_RS = 40;                  // smem row stride: halo-left at 3, interior 4..35, halo-right 36
@@ -395,6 +396,37 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
   for (int i = 0; i < L0_AHEAD; ++i)
     stage(i, z0 - 1 + i, ((F >> i) & 0xf) != 0, i == 0 ? z0 - 1 : z0 + i, min(z0 + i, z1));
 
+  // interface pass of plane t: 8 tasks (node of the plane's list, incident
+  // element e = task & 7) per listed node; the voxel scale of task j (0 past
+  // the list)
+  auto if_tasks = [&](int t) -> int {
+    int c = 0;
+    if (t >= z0 && t < z1)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) c += s_cnt[t & 1][w];
+    return 8 * c;
+  };
+  auto if_node = [&](int t, int jn) -> int {
+    int nt = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {                      // node jn -> (warp w, entry)
+      const int c = s_cnt[t & 1][w];
+      if (jn >= 0 && jn < c) nt = s_list[t & 1][w][jn];
+      jn -= c;
+    }
+    return nt;
+  };
+  auto if_scale = [&](int t, int j, int ntask) -> float {
+    if (j >= ntask) return 0.f;
+    const int nt = if_node(t, j >> 3), e = j & 7;
+    int gx = x0 + nt % L0_X - 1 + (e & 1), gy = y0 + nt / L0_X - 1 + ((e >> 1) & 1);
+    if (TL != L0_INNER) {                               // interior tiles: no wrap
+      gx = wrapi(gx, n);
+      gy = wrapi(gy, n);
+    }
+    return __ldg(s + (ptrdiff_t)zs(t - 1 + (e >> 2)) * plane + (ptrdiff_t)gy * n + gx);
+  };
+
   const int ca_off = 2 * ty * L0_X + tx;               // own node a in a code plane
   float ca_prev = 0.f, cb_prev = 0.f;                  // codes of plane p-1 (nodes a, b)
   float ca_cur = 0.f, cb_cur = 0.f;                    // plane p (read after the first barrier)
@@ -414,6 +446,9 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
       }
     }
     __syncthreads();   // plane p staged; iteration p-1 done: its ring slot and interface list are free
+#ifndef L0_NO_IFACE
+    const float se_pf = if_scale(p - 2, tid, if_tasks(p - 2));   // round 0 of this iteration's interface pass
+#endif
     {
       const int pl = p + L0_AHEAD, sl = sl_add(sl_p, L0_AHEAD);
       if (pl <= z1) stage(sl, pl, ((F >> L0_AHEAD) & 0xf) != 0, pl + 1, min(pl + 1, z1));
@@ -572,37 +607,24 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
     }
 
 #ifndef L0_NO_IFACE
-    // ---- interface nodes of plane t = p - 2 (listed last iteration), 8 lanes
-    // per node, one per incident element; planes t-1 .. t+1 are resident
+    // ---- interface nodes of plane t = p - 2 (listed last iteration): 8 lanes
+    // per node, one per incident element e; planes t-1 .. t+1 are resident.
+    // The scales of round 0 were loaded before the uniform stencil (se_pf),
+    // each round loads those of the next.
     {
       const int t = p - 2;
-      int cnt[NW], total = 0;
-      if (t >= z0 && t < z1) {
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          cnt[w] = s_cnt[t & 1][w];
-          total += cnt[w];
-        }
-      }
-      const int ntask = 8 * total;
+      const int ntask = if_tasks(t);
       const int sl_t = sl_add(sl_p, -2);
+      float se = se_pf;
       for (int j0 = 0; j0 < ntask; j0 += L0_NTH) {
         const int j = j0 + tid;
         const bool act = j < ntask;
         const int e = j & 7;
-        int jn = j >> 3, nt = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {                  // node jn -> (warp w, entry)
-          if (jn >= 0 && jn < cnt[w]) nt = s_list[t & 1][w][jn];
-          jn -= cnt[w];
-        }
+        const int nt = if_node(t, j >> 3);
+        const float se_nx = if_scale(t, j + L0_NTH, ntask);
         const int ntx_ = nt % L0_X, nty_ = nt / L0_X;   // node (ntx_, nty_) of the 32 x 8 tile
         const int ex = e & 1, ey = (e >> 1) & 1, ez = e >> 2;
         const float tX = ex ? 1.f : -1.f, tY = ey ? 1.f : -1.f, tZ = ez ? 1.f : -1.f;
-        const int gx = x0 + ntx_, gy = y0 + nty_;
-        float se = 0.f;
-        if (act) se = __ldg(s + (ptrdiff_t)zs(t - 1 + ez) * plane + (ptrdiff_t)wrapi(gy - 1 + ey, n) * n +
-                            wrapi(gx - 1 + ex, n));
         // -(s_e K_e u_e) at the node's corner (difference form) and s_e f_e
         T racc[DPN], facc[DPN];
 #pragma unroll
@@ -646,7 +668,8 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
             }
           }
         }
-        // 8-lane reduction (fixed xor tree: deterministic)
+        // 8-lane butterfly (fixed xor tree: deterministic); every lane of the
+        // node ends with the totals
         float ssum = se;
 #pragma unroll
         for (int msk = 1; msk < 8; msk <<= 1) {
@@ -657,27 +680,39 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
             if (!FEXP) facc[pp] = vadd(facc[pp], V::shfl_xor(facc[pp], msk));
           }
         }
-        if (act && e == 0) {
-          const ptrdiff_t node = (ptrdiff_t)t * plane + (ptrdiff_t)gy * n + gx;
+        // lane e < DPN finishes component e of the node
+        if (act && e < DPN) {
+          T rs = racc[0], fs = facc[0], us = uc[0];
+          float kd = C.kdiag[0];
 #pragma unroll
-          for (int pp = 0; pp < DPN; ++pp) {
-            const T f = FEXP ? V::ldg(fx + (ptrdiff_t)pp * cs + node, lcg) : facc[pp];
-            const T r = vadd(f, racc[pp]);
-            const float D = ssum * C.kdiag[pp];
-            T o;
-            if (MODE == M_JACOBI) o = vfma(V::splat(D > 0.f ? C.omega / D : 0.f), r, uc[pp]);
-            else o = r;
-            V::st(out + (ptrdiff_t)pp * cs + node, lcg, o);
-            if (part) {
+          for (int k = 1; k < DPN; ++k)
+            if (e == k) {
+              rs = racc[k];
+              fs = facc[k];
+              us = uc[k];
+              kd = C.kdiag[k];
+            }
+          const ptrdiff_t o_off = (ptrdiff_t)e * cs + (ptrdiff_t)t * plane + (ptrdiff_t)(y0 + nty_) * n + x0 + ntx_;
+          const T f = FEXP ? V::ldg(fx + o_off, lcg) : fs;
+          const T r = vadd(f, rs);
+          T o;
+          if (MODE == M_JACOBI) {
+            const float D = ssum * kd;
+            o = vfma(V::splat(D > 0.f ? C.omega * __frcp_rn(D) : 0.f), r, us);
+          } else {
+            o = r;
+          }
+          V::st(out + o_off, lcg, o);
+          if (part) {
 #pragma unroll
-              for (int jj = 0; jj < NRG; ++jj) {
-                const double rv = V::lane(r, jj), fv = V::lane(f, jj);
-                nrm[jj] += rv * rv;
-                nrm[NRG + jj] += fv * fv;
-              }
+            for (int jj = 0; jj < NRG; ++jj) {
+              const double rv = V::lane(r, jj), fv = V::lane(f, jj);
+              nrm[jj] += rv * rv;
+              nrm[NRG + jj] += fv * fv;
             }
           }
         }
+        se = se_nx;
       }
     }
 #endif
