@@ -216,16 +216,22 @@ __global__ void k_gather_stencil(const float* __restrict__ S, ptrdiff_t nodes, c
 }
 
 // Coarse-level interface nodes (ncode -1) from a sorted list: stored
-// Galerkin stencil (compact, list order), f from memory.
-template <int DPN, int MODE>
+// Galerkin stencil (compact, list order), f from memory.  Thread = (node,
+// group of NRG load cases; blockIdx.y enumerates the groups); each
+// neighbour's NRG DPN values are loaded together before its 3x3 blocks are
+// applied (memory-level parallelism: the kernel is gather-latency-bound).
+template <int DPN, int MODE, int NRG>
 __global__ void __launch_bounds__(128)
 k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu, const float* __restrict__ f,
                float* __restrict__ out, int n, int nz, float omega, ptrdiff_t cs, const int* __restrict__ list,
                int count) {
-  using T = Tr<DPN>;
-  constexpr int NR = T::NR, V = T::V;
+  constexpr int V = NRG * DPN;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
+  const ptrdiff_t go = (ptrdiff_t)blockIdx.y * V * cs;   // first component of the group
+  u += go;
+  f += go;
+  out += go;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t node = list[i];
   const int x = (int)(node % n), y = (int)((node / n) % n), z = (int)(node / plane);
@@ -236,6 +242,9 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
   for (int d = 0; d < 27; ++d) {
     const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
     const ptrdiff_t j = (ptrdiff_t)zu(z + dz) * plane + (ptrdiff_t)wrapi(y + dy, n) * n + wrapi(x + dx, n);
+    float uj[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) uj[k] = __ldg(u + k * cs + j);
 #pragma unroll
     for (int p = 0; p < DPN; ++p)
 #pragma unroll
@@ -243,11 +252,11 @@ k_coarse_iface(const float* __restrict__ S, const float* __restrict__ u, ZMap zu
         const float a = __ldg(S + (ptrdiff_t)((d * DPN + p) * DPN + q) * count + i);
         if (d == 13 && p == q) D[p] = a;
 #pragma unroll
-        for (int m = 0; m < NR; ++m) acc[m * DPN + p] = fmaf(a, __ldg(u + (m * DPN + q) * cs + j), acc[m * DPN + p]);
+        for (int m = 0; m < NRG; ++m) acc[m * DPN + p] = fmaf(a, uj[m * DPN + q], acc[m * DPN + p]);
       }
   }
-  double nrm[2 * NR];
-  op_epilogue<DPN, MODE>(true, out + node, cs, acc, fl, ui, D, omega, nrm, false);
+  double nrm[2 * Tr<DPN>::NR];
+  op_epilogue<DPN, MODE, NRG>(true, out + node, cs, acc, fl, ui, D, omega, nrm, false);
 }
 
 // One pass over the material for the level-0 setup (replaces k_tile_flags +

@@ -389,14 +389,17 @@ k_prolong_add(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int n
 // coarse value is read once per cell instead of once per fine node, and fine
 // rows move as float2 pairs (2X, 2X+1).  Cells whose 8 fine nodes are all
 // inactive (codes 0) are skipped.  nf even; nzf = 2 * (coarse planes).
-template <int DPN>
+template <int DPN, int G>
 __global__ void __launch_bounds__(128)
 k_prolong_cell(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int nf, int nzf, int nc,
                const float* __restrict__ act, ptrdiff_t csf, ptrdiff_t csc) {
-  constexpr int V = Tr<DPN>::V;
+  // blockIdx.z = Z * (V / G) + component group: G components per thread, all
+  // loads of the group issued before the first store (memory-level parallelism)
+  constexpr int V = Tr<DPN>::V, NGR = V / G;
+  static_assert(V % G == 0, "component groups");
   const int X = blockIdx.x * blockDim.x + threadIdx.x;
   const int Y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int Z = blockIdx.z;                            // fine planes 2Z, 2Z+1
+  const int Z = blockIdx.z / NGR, q0 = (blockIdx.z - Z * NGR) * G;   // fine planes 2Z, 2Z+1
   const bool valid = X < nc && Y < nc;
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   // fine rows (j, k): base index of the pair (2X, 2X+1)
@@ -417,16 +420,25 @@ k_prolong_cell(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int 
   const ptrdiff_t Z0 = (ptrdiff_t)zc(Z) * pc, Z1 = (ptrdiff_t)zc(Z + 1) * pc;
   const ptrdiff_t c00 = (ptrdiff_t)Y * nc + X, c10 = (ptrdiff_t)Y * nc + X1;
   const ptrdiff_t c01 = (ptrdiff_t)Y1 * nc + X, c11 = (ptrdiff_t)Y1 * nc + X1;
-#pragma unroll 3
-  for (int q = 0; q < V; ++q) {
-    const float* ec = e + q * csc;
-    // coarse corners [z][y][x]
-    float c[2][2][2];
-    c[0][0][0] = __ldg(ec + Z0 + c00); c[0][0][1] = __ldg(ec + Z0 + c10);
-    c[0][1][0] = __ldg(ec + Z0 + c01); c[0][1][1] = __ldg(ec + Z0 + c11);
-    c[1][0][0] = __ldg(ec + Z1 + c00); c[1][0][1] = __ldg(ec + Z1 + c10);
-    c[1][1][0] = __ldg(ec + Z1 + c01); c[1][1][1] = __ldg(ec + Z1 + c11);
-    float* uq = u + q * csf;
+  // coarse corners [q][z][y][x] and fine rows [q][k][j] of the group
+  float c[G][2][2][2];
+  float2 v[G][2][2];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float* ec = e + (q0 + g) * csc;
+    c[g][0][0][0] = __ldg(ec + Z0 + c00); c[g][0][0][1] = __ldg(ec + Z0 + c10);
+    c[g][0][1][0] = __ldg(ec + Z0 + c01); c[g][0][1][1] = __ldg(ec + Z0 + c11);
+    c[g][1][0][0] = __ldg(ec + Z1 + c00); c[g][1][0][1] = __ldg(ec + Z1 + c10);
+    c[g][1][1][0] = __ldg(ec + Z1 + c01); c[g][1][1][1] = __ldg(ec + Z1 + c11);
+    const float* uq = u + (q0 + g) * csf;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) v[g][k][j] = *reinterpret_cast<const float2*>(uq + rowf[k][j]);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float* uq = u + (q0 + g) * csf;
 #pragma unroll
     for (int k = 0; k < 2; ++k)
 #pragma unroll
@@ -435,14 +447,14 @@ k_prolong_cell(const float* __restrict__ e, ZMap zc, float* __restrict__ u, int 
         float col[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const float z0y0 = k ? 0.5f * (c[0][0][i] + c[1][0][i]) : c[0][0][i];
-          const float z0y1 = k ? 0.5f * (c[0][1][i] + c[1][1][i]) : c[0][1][i];
+          const float z0y0 = k ? 0.5f * (c[g][0][0][i] + c[g][1][0][i]) : c[g][0][0][i];
+          const float z0y1 = k ? 0.5f * (c[g][0][1][i] + c[g][1][1][i]) : c[g][0][1][i];
           col[i] = j ? 0.5f * (z0y0 + z0y1) : z0y0;
         }
-        float2 v = *reinterpret_cast<const float2*>(uq + rowf[k][j]);
-        if (a[k][j].x != 0.f) v.x += col[0];
-        if (a[k][j].y != 0.f) v.y += 0.5f * (col[0] + col[1]);
-        *reinterpret_cast<float2*>(uq + rowf[k][j]) = v;
+        float2 w = v[g][k][j];
+        if (a[k][j].x != 0.f) w.x += col[0];
+        if (a[k][j].y != 0.f) w.y += 0.5f * (col[0] + col[1]);
+        *reinterpret_cast<float2*>(uq + rowf[k][j]) = w;
       }
   }
 }
