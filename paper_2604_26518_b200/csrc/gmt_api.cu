@@ -361,8 +361,9 @@ bool l0_attrs(int bytes) {
 }
 
 template <int DPN>
+// [zlo, zhi): target planes of a level-0 V-cycle sweep (default all).
 int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, float* out, double* part,
-              int skip_void = 0) {
+              int skip_void = 0, int zlo = 0, int zhi = -1) {
   const LevelBuf& b = p->lv[l];
   const Geo g = geo(b.n, b.nz);
   cudaStream_t st = p->stream;
@@ -390,7 +391,11 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
   } else if (l == 0 && skip_void && (mode == M_JACOBI || mode == M_RESID)) {
     // the V-cycle's level-0 sweep: uniform + interface nodes in one launch
     const ZMap z = p->zm(0);
-    const dim3 grid = l0_grid<DPN>(p), block(L0_X, L0_TY);
+    if (zhi < 0) zhi = b.nz;
+    if (zlo < 0 || zhi > b.nz || zlo >= zhi) return fail(GMT_ERR_ARG, "bad plane range");
+    dim3 grid = l0_grid<DPN>(p);
+    grid.z = (unsigned)(((zhi - zlo + L0_ZC - 1) / L0_ZC) * (Tr<DPN>::NR / L0V<DPN>::NRG));
+    const dim3 block(L0_X, L0_TY);
     const size_t shm = l0_smem<DPN>();
     const float* s0 = p->s;
     const CUtensorMap* tmu = nullptr;
@@ -405,17 +410,17 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
       if (f) {
         if (mode == M_JACOBI)
           k_l0<DPN, M_JACOBI, true, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
-                                                               p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg);
+                                                               p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg, zlo, zhi);
         else
           k_l0<DPN, M_RESID, true, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
-                                                              p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg);
+                                                              p->tflag, p->tntx, p->tnty, f, tm, p->tm_code, zg, zlo, zhi);
       } else {
         if (mode == M_JACOBI)
           k_l0<DPN, M_JACOBI, false, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
-                                                                p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg);
+                                                                p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg, zlo, zhi);
         else
           k_l0<DPN, M_RESID, false, TL><<<g, block, shm, st>>>(p->code, s0, z, u, z, out, b.n, b.nz, p->l0c, pt, cs,
-                                                               p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg);
+                                                               p->tflag, p->tntx, p->tnty, nullptr, tm, p->tm_code, zg, zlo, zhi);
       }
     };
     // the split pays when interior tiles dominate (>= 256 nodes across)

@@ -86,7 +86,7 @@ k_coarse_tiled(const float* __restrict__ code, ZMap zs, const float* __restrict_
   // tile flags of voxel planes z0-3 .. z0+ZC+1: one flag per lane, one ballot
   static_assert(TT_ZC + 5 <= 32, "flag window must fit a warp");
   const int lane = tid & 31;
-  const bool fl_on = lane < TT_ZC + 5 &&
+  const bool fl_on = lane < TT_ZC + 5 && z0 - 3 + lane <= z1 + 1 &&   // a slab's flags end at plane z1 + 1
                      flag[((ptrdiff_t)zs(z0 - 3 + lane) * nty + blockIdx.y) * ntx + blockIdx.x] != 0;
   const unsigned fm = __ballot_sync(0xffffffffu, fl_on);
   auto vflag = [&](int zv) -> bool { return (fm >> (zv - z0 + 3)) & 1u; };

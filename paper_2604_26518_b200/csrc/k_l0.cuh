@@ -191,7 +191,9 @@ __device__ __forceinline__ float l0_tau(int m, float tx, float ty, float tz) {
 
 // MODE: M_JACOBI (out = u + omega D^-1 (f - K u)) or M_RESID (out = f - K u).
 // FEXP: f read from f_all (iterative refinement defect) instead of the element
-// loads.  blockIdx.z = z-chunk * NG + load-case group.  part (optional): per
+// loads.  Target planes [zlo, zhi) (a slab's interior or boundary planes when
+// the halo exchange overlaps the sweep; else [0, nz)); blockIdx.z = z-chunk *
+// NG + load-case group (chunks of L0_ZC planes from zlo).  part (optional): per
 // CTA 2 * NR doubles, sum r^2 then sum f^2 per load case.
 // TL selects the tiles of the launch: L0_ALL (every tile, cp.async staging),
 // L0_INNER (tiles whose staged box lies inside the grid: TMA staging, grid
@@ -203,7 +205,8 @@ __global__ void __launch_bounds__(L0_NTH, 4)
 k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const float* __restrict__ u_all, ZMap zu,
      float* __restrict__ out_all, int n, int nz, const L0Consts C, double* __restrict__ part, ptrdiff_t cs,
      const uint8_t* __restrict__ flag, int ntx, int nty4, const float* __restrict__ f_all,
-     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_code, int zg) {
+     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_code, int zg, int zlo,
+     int zhi) {
   static_assert(MODE == M_JACOBI || MODE == M_RESID, "level-0 sweep: V-cycle modes only");
   using V = L0V<DPN>;
   using T = typename V::T;
@@ -252,7 +255,7 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
     }
   }
   const int x0 = bx * L0_X, y0 = by * L0_Y;
-  const int z0 = chunk * L0_ZC, z1 = min(nz, z0 + L0_ZC);
+  const int z0 = zlo + chunk * L0_ZC, z1 = min(zhi, z0 + L0_ZC);   // target planes of the CTA
   const int x = x0 + tx, ya = y0 + 2 * ty;      // nodes (x, ya) and (x, ya + 1)
   const bool va = x < n && ya < n, vb = x < n && ya + 1 < n;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
@@ -268,8 +271,11 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
     if (t4 + 1 < nty4) a |= flag[(r + t4 + 1) * ntx + bx] != 0;
     return a;
   };
-  unsigned long long fm = __ballot_sync(0xffffffffu, tflag(z0 - 3 + lane));
-  fm |= (unsigned long long)__ballot_sync(0xffffffffu, lane < L0_ZC + 5 - 32 && tflag(z0 + 29 + lane)) << 32;
+  // (only voxel planes <= z1 + 1 are ever consulted; a slab's flags end there)
+  unsigned long long fm = __ballot_sync(0xffffffffu, z0 - 3 + lane <= z1 + 1 && tflag(z0 - 3 + lane));
+  fm |= (unsigned long long)__ballot_sync(0xffffffffu, lane < L0_ZC + 5 - 32 && z0 + 29 + lane <= z1 + 1 &&
+                                                           tflag(z0 + 29 + lane))
+        << 32;
   // F (iteration p): bit i = voxel plane p - 2 + i active
   unsigned long long F = fm;
 
