@@ -675,17 +675,24 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
           }
         }
         // 8-lane butterfly (fixed xor tree: deterministic); every lane of the
-        // node ends with the totals
+        // node ends with the totals.  Without norms only r = sum_e (s_e f_e -
+        // s_e K_e u_e) is needed: the element's two parts are added first.
+        const bool fsep = !FEXP && part != nullptr;
+        if (!FEXP && !fsep)
+#pragma unroll
+          for (int pp = 0; pp < DPN; ++pp) racc[pp] = vadd(facc[pp], racc[pp]);
         float ssum = se;
 #pragma unroll
         for (int msk = 1; msk < 8; msk <<= 1) {
           ssum += __shfl_xor_sync(0xffffffffu, ssum, msk);
 #pragma unroll
-          for (int pp = 0; pp < DPN; ++pp) {
-            racc[pp] = vadd(racc[pp], V::shfl_xor(racc[pp], msk));
-            if (!FEXP) facc[pp] = vadd(facc[pp], V::shfl_xor(facc[pp], msk));
-          }
+          for (int pp = 0; pp < DPN; ++pp) racc[pp] = vadd(racc[pp], V::shfl_xor(racc[pp], msk));
         }
+        if (fsep)
+#pragma unroll
+          for (int msk = 1; msk < 8; msk <<= 1)
+#pragma unroll
+            for (int pp = 0; pp < DPN; ++pp) facc[pp] = vadd(facc[pp], V::shfl_xor(facc[pp], msk));
         // lane e < DPN finishes component e of the node
         if (act && e < DPN) {
           T rs = racc[0], fs = facc[0], us = uc[0];
@@ -699,8 +706,8 @@ k_l0(const float* __restrict__ code, const float* __restrict__ s, ZMap zs, const
               kd = C.kdiag[k];
             }
           const ptrdiff_t o_off = (ptrdiff_t)e * cs + (ptrdiff_t)t * plane + (ptrdiff_t)(y0 + nty_) * n + x0 + ntx_;
-          const T f = FEXP ? V::ldg(fx + o_off, lcg) : fs;
-          const T r = vadd(f, rs);
+          const T f = FEXP ? V::ldg(fx + o_off, lcg) : (fsep ? fs : V::zero());
+          const T r = FEXP || fsep ? vadd(f, rs) : rs;
           T o;
           if (MODE == M_JACOBI) {
             const float D = ssum * kd;
