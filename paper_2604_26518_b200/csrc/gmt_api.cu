@@ -202,6 +202,7 @@ struct gmt_problem_s {
 // Ghost planes of the level-0 per-voxel / per-node arrays (allocated in every
 // mode; used when slab-partitioned).
 constexpr int MAT_GLO = 2, MAT_GHI = 1;   // material: voxel planes -2..-1, nz
+constexpr int COARSEST_SMEM_MAX = 96 * 1024;   // k_coarsest_smem: both vectors of the coarsest level
 constexpr int TF_GLO = 3, TF_GHI = 2;     // tile flags: planes -3..-1, nz..nz+1 (set to 1 = active)
 
 namespace {
@@ -554,7 +555,14 @@ int coarsest(gmt_problem p) {
   const int sweeps = p->cfg.coarse_sweeps;
   if (l == 0 || b.nodes > 32768) return smooth<DPN>(p, l, sweeps);
   Prof prof(p, 5);
-  k_coarsest<DPN><<<1, 1024, 0, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps, (float)p->cfg.omega, b.ncode, b.Hl);
+  const size_t shm = 2 * (size_t)Tr<DPN>::V * b.nodes * sizeof(float);
+  const size_t shs = (size_t)27 * DPN * DPN * b.nodes * sizeof(float);
+  const int stage_S = shm + shs <= (size_t)COARSEST_SMEM_MAX;
+  if (shm <= (size_t)COARSEST_SMEM_MAX)
+    k_coarsest_smem<DPN><<<1, 1024, stage_S ? shm + shs : shm, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps,
+                                                                          (float)p->cfg.omega, b.ncode, b.Hl, stage_S);
+  else
+    k_coarsest<DPN><<<1, 1024, 0, p->stream>>>(b.S, b.f, b.u, b.t, b.n, sweeps, (float)p->cfg.omega, b.ncode, b.Hl);
   LAUNCHED(p);
   return GMT_OK;
 }
@@ -1333,6 +1341,8 @@ int create_impl(const gmt_config* cfg_in, int P, int rank, cudaStream_t shared_s
         cudaFuncSetAttribute(k_coarse_tiled<1, M_JACOBI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         cudaFuncSetAttribute(k_coarse_tiled<1, M_RESID, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, shm1) ||
         l0_attrs<3>(l3) || l0_attrs<1>(l1) ||
+        cudaFuncSetAttribute(k_coarsest_smem<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, COARSEST_SMEM_MAX) ||
+        cudaFuncSetAttribute(k_coarsest_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, COARSEST_SMEM_MAX) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_RESID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||
         cudaFuncSetAttribute(k_l0_tc<3, M_JACOBI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem_bytes<3>()) ||

@@ -516,4 +516,71 @@ k_coarsest(const float* __restrict__ S, const float* __restrict__ f, float* u, f
   }
 }
 
+// Coarsest level, small grids (nodes * V floats x 2 fit in shared memory):
+// the ping-pong vectors (and, if they fit too, the stored stencils) live in
+// shared memory for all sweeps and the work is spread over (node, load case)
+// tasks, so a sweep is a few shared-memory round trips instead of a chain of
+// L2 gathers per node (k_coarsest keeps one thread per node).  Same
+// arithmetic per output as k_coarsest.
+template <int DPN>
+__global__ void __launch_bounds__(1024)
+k_coarsest_smem(const float* __restrict__ S, const float* __restrict__ f, float* u, float* t, int n, int sweeps,
+                float omega, const float* __restrict__ ncd, const float* __restrict__ Hl, int stage_S) {
+  constexpr int NR = Tr<DPN>::NR, V = Tr<DPN>::V, NE = 27 * DPN * DPN;
+  extern __shared__ float sv[];   // [2][V][nodes], then (stage_S) the stencils [NE][nodes]
+  const int nodes = n * n * n;
+  float* a = sv;
+  float* b = sv + V * nodes;
+  for (int i = threadIdx.x; i < V * nodes; i += blockDim.x) a[i] = u[i];
+  if (stage_S) {
+    float* ss = sv + 2 * V * nodes;
+    for (int i = threadIdx.x; i < NE * nodes; i += blockDim.x) ss[i] = S[i];
+    S = ss;
+  }
+  __syncthreads();
+  const int ntask = nodes * NR;
+  for (int it = 0; it < sweeps; ++it) {
+    const float* src = (it & 1) ? b : a;
+    float* dst = (it & 1) ? a : b;
+    for (int task = threadIdx.x; task < ntask; task += blockDim.x) {
+      const int i = task % nodes, m = task / nodes;
+      const int x = i % n, y = (i / n) % n, z = i / (n * n);
+      const float c = ncd[i];
+      float acc[DPN];
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) acc[p] = 0.f;
+#pragma unroll
+      for (int d = 0; d < 27; ++d) {
+        const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+        const int j = (wrapi(z + dz, n) * n + wrapi(y + dy, n)) * n + wrapi(x + dx, n);
+        float uj[DPN];
+#pragma unroll
+        for (int q = 0; q < DPN; ++q) uj[q] = src[(m * DPN + q) * nodes + j];
+#pragma unroll
+        for (int p = 0; p < DPN; ++p)
+#pragma unroll
+          for (int q = 0; q < DPN; ++q) {
+            const int k = (d * DPN + p) * DPN + q;
+            const float A = c >= 0.f ? c * __ldg(Hl + k) : S[(ptrdiff_t)k * nodes + i];
+            acc[p] = fmaf(A, uj[q], acc[p]);
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < DPN; ++p) {
+        const int k = m * DPN + p;
+        const int kd = (13 * DPN + p) * DPN + p;
+        const float Dp = c >= 0.f ? c * __ldg(Hl + kd) : S[(ptrdiff_t)kd * nodes + i];
+        const float ui = src[k * nodes + i];
+        dst[k * nodes + i] = Dp > 0.f ? fmaf(omega / Dp, __ldg(f + k * nodes + i) - acc[p], ui) : ui;
+      }
+    }
+    __syncthreads();
+  }
+  const float* fin = (sweeps & 1) ? b : a;
+  for (int i = threadIdx.x; i < V * nodes; i += blockDim.x) {
+    u[i] = fin[i];
+    if (sweeps & 1) t[i] = fin[i];
+  }
+}
+
 }  // namespace gmt
