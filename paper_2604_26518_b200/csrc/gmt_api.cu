@@ -680,11 +680,19 @@ int build_operators(gmt_problem p) {
       }
     }
     LevelBuf& b = p->lv[1];
-    const Geo g = geo(b.n, b.nz);
     Prof prof(p, 6);
-    k_stencil_l1<DPN><<<dim3(g.grid.x, g.grid.y, g.grid.z * 3), g.block, 0, st>>>(p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz,
-                                                  (float)p->ed.lam, (float)p->ed.mu, b.ncode);
-    LAUNCHED(p);
+    if (b.tiled) {   // the interface list exists: one thread per (interface node, offset group)
+      if (b.icount > 0) {
+        k_stencil_l1_list<DPN><<<dim3((b.icount + 127) / 128, 3), 128, 0, st>>>(
+            p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, (float)p->ed.lam, (float)p->ed.mu, b.ilist, b.icount);
+        LAUNCHED(p);
+      }
+    } else {
+      const Geo g = geo(b.n, b.nz);
+      k_stencil_l1<DPN><<<dim3(g.grid.x, g.grid.y, g.grid.z * 3), g.block, 0, st>>>(
+          p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, (float)p->ed.lam, (float)p->ed.mu, b.ncode);
+      LAUNCHED(p);
+    }
   }
   for (int l = 2; l < L; ++l) {
     LevelBuf& b = p->lv[l];
@@ -1473,7 +1481,14 @@ int gmt_set_initial_guess(gmt_problem p, const float* u, int location) {
   p->u_ready_pending = false;
   CK(cudaStreamWaitEvent(p->copy_stream, p->ev_u_ready, 0));
   if (location == GMT_DEVICE) {
-    k_copy_active<<<1184, 256, 0, p->copy_stream>>>(p->code, u, b.u, b.nodes, b.cs, p->V);
+    const bool a16 = ((uintptr_t)u % 16 == 0) && ((uintptr_t)b.u % 16 == 0) && ((uintptr_t)p->code % 16 == 0) &&
+                     b.nodes % 4 == 0 && b.cs % 4 == 0;
+    if (a16 && p->V == 18)
+      k_copy_active4<18><<<1184, 256, 0, p->copy_stream>>>(p->code, u, b.u, b.nodes, b.cs);
+    else if (a16 && p->V == 3)
+      k_copy_active4<3><<<1184, 256, 0, p->copy_stream>>>(p->code, u, b.u, b.nodes, b.cs);
+    else
+      k_copy_active<<<1184, 256, 0, p->copy_stream>>>(p->code, u, b.u, b.nodes, b.cs, p->V);
     LAUNCHED(p);
   } else {
     TRY(copy_in(p, b, b.u, u, cudaMemcpyHostToDevice, p->copy_stream));

@@ -99,6 +99,25 @@ __global__ void k_mask_inactive(const float* __restrict__ code, float* __restric
 // reset_solution) and gmt_get_solution reports them as 0, so they are left as
 // they are -- the copy reads ~the active fraction of the guess instead of all
 // of it.  src is [V][nodes], dst [V][cs].
+// Same copy, 4 nodes per thread (16-byte rows; nodes, cs and src 16-byte
+// aligned): a group with any active node is copied whole -- the values this
+// writes at inactive nodes never matter (see above) -- all-void groups are
+// skipped.  All 18 (or 3) loads of a thread are issued before its stores.
+template <int V>
+__global__ void k_copy_active4(const float* __restrict__ code, const float* __restrict__ src,
+                               float* __restrict__ dst, size_t nodes, ptrdiff_t cs) {
+  const size_t n4 = nodes / 4;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n4; g += (size_t)gridDim.x * blockDim.x) {
+    const float4 c = __ldg(reinterpret_cast<const float4*>(code) + g);
+    if (c.x == 0.f && c.y == 0.f && c.z == 0.f && c.w == 0.f) continue;
+    float4 v[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(src + (size_t)k * nodes) + g);
+#pragma unroll
+    for (int k = 0; k < V; ++k) reinterpret_cast<float4*>(dst + (ptrdiff_t)k * cs)[g] = v[k];
+  }
+}
+
 __global__ void k_copy_active(const float* __restrict__ code, const float* __restrict__ src,
                               float* __restrict__ dst, size_t nodes, ptrdiff_t cs, int V) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nodes; i += (size_t)gridDim.x * blockDim.x) {
@@ -171,19 +190,11 @@ __device__ __forceinline__ void l1_group(std::integer_sequence<int, Ds...>, cons
   (l1_block<DPN, 9 * G + Ds>(sv, lam, mu, S, nodes, node), ...);
 }
 
-// grid.z = 3 * nzc: block (., ., 3 Z + g) computes the offsets of dz = g - 1
-// of plane Z, so consecutive CTAs share one group's code.
+// Level-1 stencil of interface node (X, Y, Z), offsets of dz = grp - 1.
 template <int DPN>
-__global__ void __launch_bounds__(128)
-k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc,
-             float lam, float mu, const float* __restrict__ ncd) {
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int Z = blockIdx.z / 3, grp = blockIdx.z % 3;
-  if (X >= nc || Y >= nc) return;
-  const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
+__device__ __forceinline__ void l1_node(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc,
+                                        ptrdiff_t nodes, int X, int Y, int Z, int grp, float lam, float mu) {
   const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
-  if (__ldg(ncd + node) >= 0.f) return;        // uniform / void node: c H_1, nothing stored
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   float sv[64];
 #pragma unroll
@@ -199,6 +210,37 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
   if (grp == 0) l1_group<DPN, 0>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
   else if (grp == 1) l1_group<DPN, 1>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
   else l1_group<DPN, 2>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
+}
+
+// grid.z = 3 * nzc: block (., ., 3 Z + g) computes the offsets of dz = g - 1
+// of plane Z, so consecutive CTAs share one group's code.
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc,
+             float lam, float mu, const float* __restrict__ ncd) {
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z = blockIdx.z / 3, grp = blockIdx.z % 3;
+  if (X >= nc || Y >= nc) return;
+  const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
+  const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
+  if (__ldg(ncd + node) >= 0.f) return;        // uniform / void node: c H_1, nothing stored
+  l1_node<DPN>(s, zs, nf, S, nc, nodes, X, Y, Z, grp, lam, mu);
+}
+
+// The same over the sorted interface-node list of level 1 (tiled levels have
+// it before the stencils): blockIdx.y = offset group, every thread of a warp
+// busy (the grid form above runs ~40 idle threads per interface node).
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_stencil_l1_list(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc, float lam,
+                  float mu, const int* __restrict__ list, int count) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
+  const int node = __ldg(list + j);
+  const int X = node % nc, Y = (node / nc) % nc, Z = node / (nc * nc);
+  l1_node<DPN>(s, zs, nf, S, nc, nodes, X, Y, Z, blockIdx.y, lam, mu);
 }
 
 // Level-2 Galerkin element matrices straight from the material:
