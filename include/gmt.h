@@ -296,6 +296,21 @@ GMT_API int gmt_op_effective_tensor(gmt_problem p, const float* u, double* CH);
  * info[3] = L.  Host only.  GMT_ERR_ARG if the partition is not possible. */
 GMT_API int gmt_slab_layout(int res, int levels, int nslabs, int rank, int* info);
 
+/* The ghost-plane exchange part `rank` of `nslabs` takes part in (row A11):
+ * the list the NCCL transport issues inside one ncclGroupStart/End (and the
+ * local transport resolves to device copies) for a vector view of nz owned
+ * planes, ncomp components `cstride` elements apart and `plane` elements per
+ * plane, with `lo` ghost planes below and `hi` above (periodic ring of parts;
+ * lo, hi in {0, 1, 2}).  Entry i: send (is_send[i] = 1) or receive of
+ * count[i] elements at element offset offset[i] from the view base (plane 0
+ * of component 0; ghost planes at plane indices -lo .. -1 and nz .. nz+hi-1)
+ * to / from part peer[i].  The sends and receives of a pair of parts match
+ * in issue order (NCCL's rule).  Returns the number of entries (at most cap
+ * are written; call with cap = 0 to size), negative on bad arguments.  Host
+ * only, no device work. */
+GMT_API int gmt_halo_schedule(int nslabs, int rank, int nz, int ncomp, long long cstride, long long plane, int lo,
+                              int hi, int* peer, int* is_send, long long* offset, long long* count, int cap);
+
 /* P slabs on one device (cfg->device), exchanging ghost planes by device
  * copies on one stream: the partitioned algorithm without a second GPU.
  * material: the full N^3 field.  The returned handle owns all slabs. */

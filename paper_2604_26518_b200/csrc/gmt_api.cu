@@ -2055,6 +2055,24 @@ int gmt_slab_layout(int res, int levels, int nslabs, int rank, int* info) {
   return GMT_OK;
 }
 
+int gmt_halo_schedule(int nslabs, int rank, int nz, int ncomp, long long cstride, long long plane, int lo, int hi,
+                      int* peer, int* is_send, long long* offset, long long* count, int cap) {
+  if (nslabs < 1 || rank < 0 || rank >= nslabs || nz < 1 || ncomp < 1 || plane < 1 || lo < 0 || hi < 0 ||
+      lo > 2 || hi > 2 || lo > nz || hi > nz || cstride < (long long)(nz + lo + hi) * plane || cap < 0 ||
+      (cap > 0 && (!peer || !is_send || !offset || !count)))
+    return fail(GMT_ERR_ARG, "bad argument");
+  View v{nullptr, 1, (ptrdiff_t)cstride, (ptrdiff_t)plane, ncomp, nz};   // esize 1: offsets in elements
+  std::vector<Xfer> ops;
+  halo_schedule(v, lo, hi, rank, nslabs, ops);
+  for (int i = 0; i < (int)ops.size() && i < cap; ++i) {
+    peer[i] = ops[i].peer;
+    is_send[i] = ops[i].send ? 1 : 0;
+    offset[i] = (long long)ops[i].off;
+    count[i] = (long long)ops[i].bytes;
+  }
+  return (int)ops.size();
+}
+
 int gmt_create_slabs(const gmt_config* cfg, const void* material, int material_dtype, int material_location,
                      int nslabs, gmt_problem* out) {
   return g_create(cfg, material, material_dtype, material_location, nslabs, 0, nullptr, out);

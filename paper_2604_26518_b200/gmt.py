@@ -76,6 +76,9 @@ SIGNATURES = {
     "gmt_op_stencil": (C.c_int, [_P, C.c_int, _FP]),
     "gmt_op_effective_tensor": (C.c_int, [_P, _FP, _DP]),
     "gmt_slab_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "gmt_halo_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_longlong, C.c_int, C.c_int,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_longlong), C.c_int]),
     "gmt_create_slabs": (C.c_int, [C.POINTER(gmt_config), C.c_void_p, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_void_p)]),
     "gmt_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
@@ -172,6 +175,19 @@ def gmt_slab_layout(res: int, levels: int, nslabs: int, rank: int) -> dict:
     info = (C.c_int * 4)()
     _check(lib.gmt_slab_layout(res, levels, nslabs, rank, info), "gmt_slab_layout")
     return {"z0": info[0], "nz": info[1], "Ld": info[2], "L": info[3]}
+
+
+def gmt_halo_schedule(nslabs: int, rank: int, nz: int, ncomp: int, cstride: int, plane: int, lo: int,
+                      hi: int) -> list:
+    """Ghost-plane exchange of one part (host only): [(peer, is_send, offset,
+    count)] in issue order, offsets / counts in elements of the view."""
+    lib = load()
+    n = lib.gmt_halo_schedule(nslabs, rank, nz, ncomp, cstride, plane, lo, hi, None, None, None, None, 0)
+    _check(n if n < 0 else 0, "gmt_halo_schedule")
+    peer, snd = (C.c_int * max(n, 1))(), (C.c_int * max(n, 1))()
+    off, cnt = (C.c_longlong * max(n, 1))(), (C.c_longlong * max(n, 1))()
+    lib.gmt_halo_schedule(nslabs, rank, nz, ncomp, cstride, plane, lo, hi, peer, snd, off, cnt, n)
+    return [(peer[i], bool(snd[i]), off[i], cnt[i]) for i in range(n)]
 
 
 def gmt_nccl_unique_id() -> bytes:

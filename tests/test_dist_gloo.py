@@ -93,3 +93,78 @@ def test_gather_level_knob(monkeypatch):
     assert gmt.gmt_slab_layout(32, 4, 4, 0)["Ld"] == 3      # falls back to >= 2 planes
     monkeypatch.delenv("GMT_SLAB_MIN_PLANES")
     assert gmt.gmt_slab_layout(512, 0, 8, 3)["Ld"] == 6
+
+
+def _halo_worker(rank, world, port, q, lo, hi):
+    """Run gmt_halo_schedule's list with gloo isend/irecv on CPU buffers (the
+    NCCL transport issues the same list in one group) and check every ghost
+    plane against the neighbour part's boundary plane."""
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_2604_26518_b200 import gmt
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        nz, ncomp, plane = 5, 3, 12
+        gl, gh = 2, 2                                   # allocated ghost planes per side
+        cstride = (gl + nz + gh) * plane
+        base = gl * plane                               # view base: plane 0 of component 0
+        buf = torch.full((ncomp * cstride,), -1.0, dtype=torch.float64)
+
+        def value(owner, c, z, i):                      # global plane owner * nz + z
+            return 1e6 * owner + 1e4 * c + 100 * z + i
+
+        for c in range(ncomp):
+            for z in range(nz):
+                s0 = base + c * cstride + z * plane
+                buf[s0:s0 + plane] = torch.tensor([value(rank, c, z, i) for i in range(plane)],
+                                                  dtype=torch.float64)
+        ops = gmt.gmt_halo_schedule(world, rank, nz, ncomp, cstride, plane, lo, hi)
+        assert len(ops) == 2 * ncomp * (lo + hi), ops
+        reqs = []
+        for peer, snd, off, cnt in ops:
+            view = buf[base + off:base + off + cnt]     # contiguous plane slices of buf
+            reqs.append(dist.isend(view.clone(), dst=peer) if snd else None)
+            if not snd:
+                recv = torch.empty(cnt, dtype=torch.float64)
+                reqs[-1] = (dist.irecv(recv, src=peer), view, recv)
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+                r[1].copy_(r[2])
+            else:
+                r.wait()
+        dn, up = (rank - 1) % world, (rank + 1) % world
+        for c in range(ncomp):
+            for g in range(1, lo + 1):                  # lower ghosts = lower part's top planes
+                s0 = base + c * cstride - g * plane
+                want = [value(dn, c, nz - g, i) for i in range(plane)]
+                assert buf[s0:s0 + plane].tolist() == want, ("lo", c, g)
+            for g in range(hi):                         # upper ghosts = upper part's bottom planes
+                s0 = base + c * cstride + (nz + g) * plane
+                want = [value(up, c, g, i) for i in range(plane)]
+                assert buf[s0:s0 + plane].tolist() == want, ("hi", c, g)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, f"{e!r}\n{traceback.format_exc()}"))
+
+
+@pytest.mark.parametrize("world,lo,hi", [(2, 1, 1), (3, 1, 1), (2, 1, 0), (3, 0, 1), (2, 2, 2)])
+def test_halo_schedule_gloo(world, lo, hi):
+    """The slab halo schedule (gmt_halo_schedule: the list the NCCL transport
+    issues) executed by `world` processes over gloo: sends and receives pair up
+    in issue order and every ghost plane ends with the neighbour part's
+    boundary plane (periodic ring; world 2 has the same part below and above)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q, lo, hi)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(60)
+    assert res == {r: "ok" for r in range(world)}, res
