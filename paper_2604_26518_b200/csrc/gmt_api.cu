@@ -454,11 +454,8 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     const ZMap z = p->zm(l);
     const dim3 grid(b.tntx, b.tnty, ((b.nz + TT_ZC - 1) / TT_ZC) * (Tr<DPN>::NR / 3)), block(TT_X, TT_Y);
     const size_t shm = (size_t)TT_NB * 3 * DPN * TT_PLS * sizeof(float);
-    // uniform nodes (tiled) and interface nodes (list) are disjoint: the
-    // interface kernel runs as a parallel branch on the aux stream
-    static const int aux_min = getenv("GMT_AUX_COARSE_MIN") ? atoi(getenv("GMT_AUX_COARSE_MIN")) : (1 << 30);
-    const bool split = b.icount > 0 && b.n >= aux_min;
-    if (split) TRY(aux_fork(p));
+    // uniform nodes (tiled), then interface nodes (list): disjoint node sets
+    // (running the two as parallel graph branches measured slower)
     if (mode == M_JACOBI)
       k_coarse_tiled<DPN, M_JACOBI, 3><<<grid, block, shm, st>>>(b.ncode, z, u, z, out, b.n, b.nz, om, cs, b.tflag,
                                                                  b.tntx, b.tnty, f, p->hc[l]);
@@ -470,14 +467,12 @@ int launch_op(gmt_problem p, int l, int mode, const float* u, const float* f, fl
     // one thread per interface node, all load cases (measured against 1, 2
     // or 3 load cases per thread: splitting repeats the coefficient loads)
     const int nbi = (b.icount + 127) / 128;
-    cudaStream_t si = split ? p->aux : st;
     constexpr int NR = Tr<DPN>::NR;
     if (mode == M_JACOBI)
-      k_coarse_iface<DPN, M_JACOBI, NR><<<nbi, 128, 0, si>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_JACOBI, NR><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
     else
-      k_coarse_iface<DPN, M_RESID, NR><<<nbi, 128, 0, si>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
+      k_coarse_iface<DPN, M_RESID, NR><<<nbi, 128, 0, st>>>(b.Si, u, z, f, out, b.n, b.nz, om, cs, b.ilist, b.icount);
     LAUNCHED(p);
-    if (split) TRY(aux_join(p));
     return GMT_OK;
   } else {
     const ZMap z = p->zm(l);
