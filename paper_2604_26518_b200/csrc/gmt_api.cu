@@ -81,7 +81,8 @@ struct LevelBuf {
   int tntx = 0, tnty = 0;
   int* ilist = nullptr;    // sorted interface nodes (ncode -1) of this coarse level
   int icount = 0;
-  float* Si = nullptr;     // their stencils in list order (k_gather_stencil)
+  float* Si = nullptr;     // their stencils in list order (k_gather_stencil / k_stencil_l1_list)
+  bool si_direct = false;  // Si written by the stencil kernel itself (level 1, single device)
   size_t si_cap = 0;       // capacity of Si in nodes
   bool inj_pending = false;
 };
@@ -590,20 +591,27 @@ int vcycle_dispatch(gmt_problem p) { return p->dpn == 3 ? vcycle_once<3>(p) : vc
 // Compact copies of the interface-node stencils of the tiled coarse levels
 // (after the stencils are assembled).  Reallocates when the list grows; the
 // captured V-cycle graph holds the pointer, so it is dropped then.
+// Capacity of a level's list-order stencil copy for its current interface count.
+int ensure_si(gmt_problem p, LevelBuf& b) {
+  const int nent = 27 * p->dpn * p->dpn;
+  if ((size_t)b.icount > b.si_cap) {
+    cudaFree(b.Si);
+    p->bytes -= b.si_cap * nent * sizeof(float);
+    b.Si = nullptr;
+    b.si_cap = 0;
+    const size_t cap = (size_t)b.icount + b.icount / 8 + 1024;
+    TRY(dalloc(p, (void**)&b.Si, cap * nent * sizeof(float)));
+    b.si_cap = cap;
+    drop_graph(p);
+  }
+  return GMT_OK;
+}
+
 int gather_iface_stencils(gmt_problem p) {
   const int nent = 27 * p->dpn * p->dpn;
   for (auto& b : p->lv) {
-    if (!b.tiled || b.icount == 0) continue;
-    if ((size_t)b.icount > b.si_cap) {
-      cudaFree(b.Si);
-      p->bytes -= b.si_cap * nent * sizeof(float);
-      b.Si = nullptr;
-      b.si_cap = 0;
-      const size_t cap = (size_t)b.icount + b.icount / 8 + 1024;
-      TRY(dalloc(p, (void**)&b.Si, cap * nent * sizeof(float)));
-      b.si_cap = cap;
-      drop_graph(p);
-    }
+    if (!b.tiled || b.icount == 0 || b.si_direct) continue;
+    TRY(ensure_si(p, b));
     k_gather_stencil<<<1184, 256, 0, p->stream>>>(b.S, (ptrdiff_t)b.nodes, b.ilist, b.icount, nent, b.Si);
     LAUNCHED(p);
   }
@@ -676,11 +684,14 @@ int build_operators(gmt_problem p) {
     }
     LevelBuf& b = p->lv[1];
     Prof prof(p, 6);
+    b.si_direct = false;
     if (b.tiled) {   // the interface list exists: one thread per (interface node, offset group)
       if (b.icount > 0) {
+        TRY(ensure_si(p, b));
         k_stencil_l1_list<DPN><<<dim3((b.icount + 127) / 128, 3), 128, 0, st>>>(
-            p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, (float)p->ed.lam, (float)p->ed.mu, b.ilist, b.icount);
+            p->s, p->zm(0), p->lv[0].n, b.S, b.n, b.nz, (float)p->ed.lam, (float)p->ed.mu, b.ilist, b.icount, b.Si);
         LAUNCHED(p);
+        b.si_direct = true;
       }
     } else {
       const Geo g = geo(b.n, b.nz);

@@ -145,7 +145,7 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ in, float* __restrict__ 
 // a compile-time constant.
 template <int DPN, int D>
 __device__ __forceinline__ void l1_block(const float (&sv)[64], float lam, float mu, float* __restrict__ S,
-                                         ptrdiff_t nodes, ptrdiff_t node) {
+                                         ptrdiff_t nodes, ptrdiff_t node, float* __restrict__ Si, int count, int j) {
   constexpr int ND = Tr<DPN>::ND;
   constexpr int dx = D % 3 - 1, dy = (D / 3) % 3 - 1, dz = D / 9 - 1;
   float Al[DPN][DPN], Am[DPN][DPN];
@@ -179,21 +179,27 @@ __device__ __forceinline__ void l1_block(const float (&sv)[64], float lam, float
   for (int p = 0; p < DPN; ++p)
 #pragma unroll
     for (int q = 0; q < DPN; ++q)
-      S[((D * DPN + p) * DPN + q) * nodes + node] = CT<DPN>::two ? fmaf(lam, Al[p][q], mu * Am[p][q]) : lam * Al[p][q];
+    {
+      const float v = CT<DPN>::two ? fmaf(lam, Al[p][q], mu * Am[p][q]) : lam * Al[p][q];
+      S[((D * DPN + p) * DPN + q) * nodes + node] = v;
+      if (Si) Si[(ptrdiff_t)((D * DPN + p) * DPN + q) * count + j] = v;   // list-order copy (k_gather_stencil's layout)
+    }
 }
 
 // The 9 offsets of one dz plane (g = dz + 1): a CTA runs one group's code,
 // a third of the 27 unrolled blocks, which keeps the instruction cache warm.
 template <int DPN, int G, int... Ds>
 __device__ __forceinline__ void l1_group(std::integer_sequence<int, Ds...>, const float (&sv)[64], float lam,
-                                         float mu, float* __restrict__ S, ptrdiff_t nodes, ptrdiff_t node) {
-  (l1_block<DPN, 9 * G + Ds>(sv, lam, mu, S, nodes, node), ...);
+                                         float mu, float* __restrict__ S, ptrdiff_t nodes, ptrdiff_t node,
+                                         float* __restrict__ Si, int count, int j) {
+  (l1_block<DPN, 9 * G + Ds>(sv, lam, mu, S, nodes, node, Si, count, j), ...);
 }
 
 // Level-1 stencil of interface node (X, Y, Z), offsets of dz = grp - 1.
 template <int DPN>
 __device__ __forceinline__ void l1_node(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc,
-                                        ptrdiff_t nodes, int X, int Y, int Z, int grp, float lam, float mu) {
+                                        ptrdiff_t nodes, int X, int Y, int Z, int grp, float lam, float mu,
+                                        float* __restrict__ Si = nullptr, int count = 0, int j = 0) {
   const ptrdiff_t node = ((ptrdiff_t)Z * nc + Y) * nc + X;
   const ptrdiff_t pf = (ptrdiff_t)nf * nf;
   float sv[64];
@@ -207,9 +213,9 @@ __device__ __forceinline__ void l1_node(const float* __restrict__ s, ZMap zs, in
       for (int fx = 0; fx < 4; ++fx) sv[(fz * 4 + fy) * 4 + fx] = __ldg(s + yo + wrapi(2 * X - 2 + fx, nf));
     }
   }
-  if (grp == 0) l1_group<DPN, 0>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
-  else if (grp == 1) l1_group<DPN, 1>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
-  else l1_group<DPN, 2>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node);
+  if (grp == 0) l1_group<DPN, 0>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node, Si, count, j);
+  else if (grp == 1) l1_group<DPN, 1>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node, Si, count, j);
+  else l1_group<DPN, 2>(std::make_integer_sequence<int, 9>{}, sv, lam, mu, S, nodes, node, Si, count, j);
 }
 
 // grid.z = 3 * nzc: block (., ., 3 Z + g) computes the offsets of dz = g - 1
@@ -230,17 +236,19 @@ k_stencil_l1(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S
 
 // The same over the sorted interface-node list of level 1 (tiled levels have
 // it before the stencils): blockIdx.y = offset group, every thread of a warp
-// busy (the grid form above runs ~40 idle threads per interface node).
+// busy (the grid form above runs ~40 idle threads per interface node); also
+// writes the list-order copy Si the tiled sweeps read (no k_gather_stencil
+// pass for this level).
 template <int DPN>
 __global__ void __launch_bounds__(128)
 k_stencil_l1_list(const float* __restrict__ s, ZMap zs, int nf, float* __restrict__ S, int nc, int nzc, float lam,
-                  float mu, const int* __restrict__ list, int count) {
+                  float mu, const int* __restrict__ list, int count, float* __restrict__ Si) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= count) return;
   const ptrdiff_t nodes = (ptrdiff_t)nc * nc * nzc;
   const int node = __ldg(list + j);
   const int X = node % nc, Y = (node / nc) % nc, Z = node / (nc * nc);
-  l1_node<DPN>(s, zs, nf, S, nc, nodes, X, Y, Z, blockIdx.y, lam, mu);
+  l1_node<DPN>(s, zs, nf, S, nc, nodes, X, Y, Z, blockIdx.y, lam, mu, Si, count, j);
 }
 
 // Level-2 Galerkin element matrices straight from the material:
