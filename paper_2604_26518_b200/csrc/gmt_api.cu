@@ -722,9 +722,20 @@ int build_operators(gmt_problem p) {
         LAUNCHED(p);
       }
     }
-    const Geo g = geo(b.n, b.nz);
-    k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode, b.ncode, b.Kh);
-    LAUNCHED(p);
+    b.si_direct = false;
+    if (b.tiled) {   // over the interface list, with the list-order copy
+      if (b.icount > 0) {
+        TRY(ensure_si(p, b));
+        k_stencil_from_elem_list<DPN><<<(b.icount + 127) / 128, 128, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode,
+                                                                              b.Kh, b.ilist, b.icount, b.Si);
+        LAUNCHED(p);
+        b.si_direct = true;
+      }
+    } else {
+      const Geo g = geo(b.n, b.nz);
+      k_stencil_from_elem<DPN><<<g.grid, g.block, 0, st>>>(b.Ke, p->zm(l), b.S, b.n, b.nz, b.ecode, b.ncode, b.Kh);
+      LAUNCHED(p);
+    }
   }
   TRY(gather_iface_stencils(p));
   return GMT_OK;

@@ -351,19 +351,16 @@ k_galerkin_elem(const float* __restrict__ src, float* __restrict__ dst, int nc, 
 
 // Assemble the 27-point block stencil of a level from its element matrices:
 //   A_I(d) = sum_{E containing I and I+d} K_E[corner_E(I), corner_E(I+d)].
+// Node (X, Y, Z); Si (optional): also the list-order copy at position j.
 template <int DPN>
-__global__ void __launch_bounds__(128)
-k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S, int n, int nz,
-                    const float* __restrict__ ecd, const float* __restrict__ ncd, const float* __restrict__ Kh) {
+__device__ __forceinline__ void stencil_from_elem_node(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S,
+                                                       int n, int nz, const float* __restrict__ ecd,
+                                                       const float* __restrict__ Kh, int X, int Y, int Z,
+                                                       float* __restrict__ Si, int count, int j) {
   constexpr int ND = Tr<DPN>::ND;
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
-  const int Z = blockIdx.z;
-  if (X >= n || Y >= n) return;
   const ptrdiff_t plane = (ptrdiff_t)n * n;
   const ptrdiff_t nodes = plane * nz;
   const ptrdiff_t node = (ptrdiff_t)Z * plane + (ptrdiff_t)Y * n + X;
-  if (__ldg(ncd + node) >= 0.f) return;         // uniform / void node: nothing stored
   ptrdiff_t eidx[8];
   float ecv[8];
   {
@@ -402,8 +399,36 @@ k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S
 #pragma unroll
     for (int p = 0; p < DPN; ++p)
 #pragma unroll
-      for (int q = 0; q < DPN; ++q) S[((d * DPN + p) * DPN + q) * nodes + node] = A[p][q];
+      for (int q = 0; q < DPN; ++q) {
+        S[((d * DPN + p) * DPN + q) * nodes + node] = A[p][q];
+        if (Si) Si[(ptrdiff_t)((d * DPN + p) * DPN + q) * count + j] = A[p][q];
+      }
   }
+}
+
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_stencil_from_elem(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S, int n, int nz,
+                    const float* __restrict__ ecd, const float* __restrict__ ncd, const float* __restrict__ Kh) {
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int Z = blockIdx.z;
+  if (X >= n || Y >= n) return;
+  if (__ldg(ncd + ((ptrdiff_t)Z * n + Y) * n + X) >= 0.f) return;   // uniform / void node: nothing stored
+  stencil_from_elem_node<DPN>(Ke, ze, S, n, nz, ecd, Kh, X, Y, Z, nullptr, 0, 0);
+}
+
+// The same over a tiled level's sorted interface list, writing the
+// list-order copy Si as well (no gather pass for the level).
+template <int DPN>
+__global__ void __launch_bounds__(128)
+k_stencil_from_elem_list(const float* __restrict__ Ke, ZMap ze, float* __restrict__ S, int n, int nz,
+                         const float* __restrict__ ecd, const float* __restrict__ Kh, const int* __restrict__ list,
+                         int count, float* __restrict__ Si) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const int node = __ldg(list + j);
+  stencil_from_elem_node<DPN>(Ke, ze, S, n, nz, ecd, Kh, node % n, (node / n) % n, node / (n * n), Si, count, j);
 }
 
 }  // namespace gmt
